@@ -1,0 +1,177 @@
+// fp64 band-field algebra and deterministic reductions (sm_100a).
+//
+// Replaces spectral.hpp:112-185 (axpy, scaled, linf_norm, all_finite,
+// band_inner), spectral.hpp:440-451 (band_divergence) and
+// spectral.hpp:518-544 (SobolevOperator::apply on band fields).  Band vectors
+// are tiny (K^3 complex per component), so these are latency-bound grid-stride
+// loops; reductions are two-pass (per-block partials, then one block in fixed
+// order) with warp-shuffle trees and fp64 accumulation, so results are
+// bit-reproducible run to run.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace lddmm_b200 {
+
+__global__ void axpby_kernel(long long n, double a, const double2* __restrict__ x, double b,
+                             const double2* __restrict__ y, double2* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 xv = x[i];
+    double2 r;
+    if (y) {
+      const double2 yv = y[i];
+      if (b == 1.0) {
+        // axpy: a*x + y evaluated like the reference (core.hpp:188-202)
+        r = make_double2(a * xv.x + yv.x, a * xv.y + yv.y);
+      } else {
+        r = make_double2(a * xv.x + b * yv.x, a * xv.y + b * yv.y);
+      }
+    } else {
+      r = make_double2(a * xv.x, a * xv.y);
+    }
+    out[i] = r;
+  }
+}
+
+void launch_axpy(long long n, double a, const double2* x, const double2* y, double2* out, cudaStream_t s) {
+  axpby_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, x, 1.0, y, out);
+  LDDMM_LAUNCH_CHECK();
+}
+void launch_axpby(long long n, double a, const double2* x, double b, const double2* y, double2* out,
+                  cudaStream_t s) {
+  axpby_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, x, b, y, out);
+  LDDMM_LAUNCH_CHECK();
+}
+void launch_scale(long long n, double a, const double2* x, double2* out, cudaStream_t s) {
+  axpby_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, x, 0.0, nullptr, out);
+  LDDMM_LAUNCH_CHECK();
+}
+
+__device__ __forceinline__ int signed_freq(int f, int K) { return f < K / 2 ? f : f - K; }
+
+__global__ void sobolev_kernel(const double2* __restrict__ in, double2* __restrict__ out, int ncomp, int Kx,
+                               int Ky, int Kz, double wx, double wy, double wz, double alpha, double s,
+                               int inverse) {
+  const long long per = (long long)Kx * Ky * Kz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per; i += (long long)gridDim.x * blockDim.x) {
+    const int fz = (int)(i % Kz);
+    const int fy = (int)((i / Kz) % Ky);
+    const int fx = (int)(i / ((long long)Kz * Ky));
+    const double ox = wx * signed_freq(fx, Kx), oy = wy * signed_freq(fy, Ky), oz = wz * signed_freq(fz, Kz);
+    double w2 = 0.0;
+    w2 += ox * ox;
+    w2 += oy * oy;
+    w2 += oz * oz;
+    double m = pow(1.0 + alpha * w2, s);
+    if (inverse) m = 1.0 / m;
+    for (int c = 0; c < ncomp; ++c) {
+      const double2 v = in[c * per + i];
+      out[c * per + i] = make_double2(v.x * m, v.y * m);
+    }
+  }
+}
+
+void launch_sobolev(const double2* in, double2* out, int ncomp, const int* K, const double* wunit, double alpha,
+                    int s, bool inverse, cudaStream_t st) {
+  const long long per = (long long)K[0] * K[1] * K[2];
+  sobolev_kernel<<<grid_for(per, 256, 4), 256, 0, st>>>(in, out, ncomp, K[0], K[1], K[2], wunit[0], wunit[1],
+                                                         wunit[2], alpha, (double)s, inverse ? 1 : 0);
+  LDDMM_LAUNCH_CHECK();
+}
+
+__global__ void divergence_kernel(const double2* __restrict__ v, double2* __restrict__ out, int Kx, int Ky, int Kz,
+                                  double wx, double wy, double wz) {
+  const long long per = (long long)Kx * Ky * Kz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per; i += (long long)gridDim.x * blockDim.x) {
+    const int fz = (int)(i % Kz);
+    const int fy = (int)((i / Kz) % Ky);
+    const int fx = (int)(i / ((long long)Kz * Ky));
+    const double om[3] = {wx * signed_freq(fx, Kx), wy * signed_freq(fy, Ky), wz * signed_freq(fz, Kz)};
+    double sx = 0.0, sy = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      const double2 c = v[a * per + i];
+      // c * (0 + i om) = (-c.y om) + i (c.x om)
+      sx += -c.y * om[a];
+      sy += c.x * om[a];
+    }
+    out[i] = make_double2(sx, sy);
+  }
+}
+
+void launch_band_divergence(const double2* v, double2* out, const int* K, const double* wunit, cudaStream_t s) {
+  const long long per = (long long)K[0] * K[1] * K[2];
+  divergence_kernel<<<grid_for(per, 256, 4), 256, 0, s>>>(v, out, K[0], K[1], K[2], wunit[0], wunit[1], wunit[2]);
+  LDDMM_LAUNCH_CHECK();
+}
+
+// ---- reductions -----------------------------------------------------------------
+
+__global__ __launch_bounds__(256) void inner_partial_kernel(long long n, const double2* __restrict__ x,
+                                                            const double2* __restrict__ y, double* part) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = x[i], b = y[i];
+    s += a.x * b.x + a.y * b.y;
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ __launch_bounds__(256) void linf_partial_kernel(long long n, const double2* __restrict__ x, double* part) {
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = x[i];
+    m = fmax(m, hypot(a.x, a.y));
+  }
+  m = block_max(m);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+__global__ __launch_bounds__(256) void nonfinite_partial_kernel(long long n, const double2* __restrict__ x,
+                                                                double* part) {
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = x[i];
+    if (!isfinite(a.x) || !isfinite(a.y)) m = 1.0;
+  }
+  m = block_max(m);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+__global__ __launch_bounds__(1024) void reduce_final_kernel(const double* __restrict__ part, int n, int op,
+                                                            double* slot) {
+  double v = op == 0 ? 0.0 : -INFINITY;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v = op == 0 ? v + part[i] : fmax(v, part[i]);
+  v = op == 0 ? block_sum(v) : block_max(v);
+  if (threadIdx.x == 0) *slot = v;
+}
+
+static int red_grid(long long n) {
+  long long g = (n + 255) / 256;
+  if (g > kReduceBlocks) g = kReduceBlocks;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int launch_inner_partial(long long n, const double2* x, const double2* y, double* part, cudaStream_t s) {
+  const int g = red_grid(n);
+  inner_partial_kernel<<<g, 256, 0, s>>>(n, x, y, part);
+  LDDMM_LAUNCH_CHECK();
+  return g;
+}
+int launch_linf_partial(long long n, const double2* x, double* part, cudaStream_t s) {
+  const int g = red_grid(n);
+  linf_partial_kernel<<<g, 256, 0, s>>>(n, x, part);
+  LDDMM_LAUNCH_CHECK();
+  return g;
+}
+int launch_nonfinite_partial(long long n, const double2* x, double* part, cudaStream_t s) {
+  const int g = red_grid(n);
+  nonfinite_partial_kernel<<<g, 256, 0, s>>>(n, x, part);
+  LDDMM_LAUNCH_CHECK();
+  return g;
+}
+void launch_reduce_final(const double* part, int nparts, int op, double* slot, cudaStream_t s) {
+  reduce_final_kernel<<<1, 1024, 0, s>>>(part, nparts, op, slot);
+  LDDMM_LAUNCH_CHECK();
+}
+
+}  // namespace lddmm_b200

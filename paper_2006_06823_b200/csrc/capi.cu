@@ -1,0 +1,368 @@
+// extern "C" implementation of include/lddmm_cuda.h over Engine / optimize.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/lddmm_cuda.h"
+#include "engine.hpp"
+#include "optimizer.hpp"
+
+using namespace lddmm_b200;
+
+struct lddmm_ctx {
+  std::unique_ptr<Engine> eng;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <class F>
+int guard(lddmm_ctx* ctx, F&& f, int* step = nullptr) {
+  try {
+    f();
+    return LDDMM_OK;
+  } catch (const EngineError& e) {
+    if (ctx) ctx->err = e.what();
+    if (step && e.status == LDDMM_EDIVERGENCE) *step = e.step;
+    return e.status;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return LDDMM_ECUDA;
+  }
+}
+
+inline double2* D2(double* p) { return reinterpret_cast<double2*>(p); }
+inline const double2* D2(const double* p) { return reinterpret_cast<const double2*>(p); }
+
+OptimizeOptions to_opts(const lddmm_options* o) {
+  OptimizeOptions r;
+  if (!o) return r;
+  r.max_iter = o->max_iter;
+  r.pcg_max_iter = o->pcg_max_iter;
+  r.pcg_tol = o->pcg_tol;
+  r.grad_tol = o->grad_tol;
+  r.energy_tol = o->energy_tol;
+  r.step_tol = o->step_tol;
+  r.armijo_c = o->armijo_c;
+  r.armijo_max_trials = o->armijo_max_trials;
+  return r;
+}
+
+void fill_result(const OptimizeResult& r, lddmm_iteration_record* hist, int cap, lddmm_result* res) {
+  if (hist) {
+    const int n = std::min<int>(cap, (int)r.history.size());
+    for (int k = 0; k < n; ++k) {
+      const IterationRecord& q = r.history[k];
+      lddmm_iteration_record& o = hist[k];
+      std::memset(&o, 0, sizeof(o));
+      o.iter = q.iter;
+      o.energy = q.energy;
+      o.energy_data = q.energy_data;
+      o.energy_reg = q.energy_reg;
+      o.mse_rel = q.mse_rel;
+      o.rel_grad = q.rel_grad;
+      o.pcg_iters = q.pcg_iters;
+      o.pcg_fallback = q.pcg_fallback ? 1 : 0;
+      o.epsilon = q.epsilon;
+      o.cfl = q.cfl;
+      o.wall_ms = q.wall_ms;
+      o.n_pcg_residuals = std::min<int>(16, (int)q.pcg_residuals.size());
+      for (int j = 0; j < o.n_pcg_residuals; ++j) o.pcg_residuals[j] = q.pcg_residuals[j];
+    }
+  }
+  if (res) {
+    res->stop_reason = r.stop;
+    res->converged = r.converged ? 1 : 0;
+    res->iterations = r.iterations;
+    res->n_history = (int)r.history.size();
+    res->final_energy = r.final_energy;
+    res->rel_grad = r.rel_grad;
+    res->hessvecs = r.hessvecs;
+    res->trials = r.trials;
+    res->forwards = r.forwards;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+void lddmm_default_options(lddmm_options* o) {
+  OptimizeOptions d;
+  o->max_iter = d.max_iter;
+  o->pcg_max_iter = d.pcg_max_iter;
+  o->pcg_tol = d.pcg_tol;
+  o->grad_tol = d.grad_tol;
+  o->energy_tol = d.energy_tol;
+  o->step_tol = d.step_tol;
+  o->armijo_c = d.armijo_c;
+  o->armijo_max_trials = d.armijo_max_trials;
+}
+
+int lddmm_create(const lddmm_problem* p, int device, lddmm_ctx** out) {
+  *out = nullptr;
+  auto ctx = std::make_unique<lddmm_ctx>();
+  const int rc = guard(ctx.get(), [&] {
+    shape_require(p != nullptr, "null problem");
+    shape_require(p->d == 3, "only 3-D grids are supported by the CUDA engine");
+    Problem q;
+    for (int a = 0; a < 3; ++a) {
+      q.dims[a] = p->dims[a];
+      q.spacing[a] = p->spacing[a];
+      q.band[a] = p->band[a];
+    }
+    q.nt = p->nt;
+    q.variant = p->variant;
+    q.stationary = p->parameterization == LDDMM_STATIONARY ? 1 : 0;
+    q.alpha = p->alpha;
+    q.s = p->s;
+    q.sigma2 = p->sigma2;
+    ctx->eng = std::make_unique<Engine>(q, device);
+  });
+  if (rc != LDDMM_OK) {
+    g_create_err = ctx->err;
+    return rc;
+  }
+  *out = ctx.release();
+  return LDDMM_OK;
+}
+
+void lddmm_destroy(lddmm_ctx* ctx) { delete ctx; }
+
+const char* lddmm_last_error(const lddmm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int lddmm_sync(lddmm_ctx* ctx) {
+  return guard(ctx, [&] { ctx->eng->sync(); });
+}
+
+long long lddmm_launch_count(void) { return launch_counter(); }
+
+int lddmm_set_images(lddmm_ctx* ctx, const double* I0, const double* I1) {
+  return guard(ctx, [&] { ctx->eng->set_images_host(I0, I1); });
+}
+
+int lddmm_set_images_dev_f32(lddmm_ctx* ctx, const float* I0, const float* I1) {
+  return guard(ctx, [&] { ctx->eng->set_images_device_f32(I0, I1); });
+}
+
+long long lddmm_velocity_doubles(const lddmm_ctx* ctx) { return 2 * ctx->eng->vel_elems(); }
+
+int lddmm_vel_alloc(lddmm_ctx* ctx, double** v) {
+  return guard(ctx, [&] {
+    const size_t bytes = ctx->eng->vel_elems() * sizeof(double2);
+    LDDMM_CUDA(cudaMalloc(v, bytes));
+    LDDMM_CUDA(cudaMemsetAsync(*v, 0, bytes, ctx->eng->stream()));
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_vel_free(lddmm_ctx* ctx, double* v) {
+  return guard(ctx, [&] { LDDMM_CUDA(cudaFree(v)); });
+}
+
+int lddmm_vel_upload(lddmm_ctx* ctx, double* dv, const double* hv) {
+  return guard(ctx, [&] {
+    LDDMM_CUDA(cudaMemcpyAsync(dv, hv, ctx->eng->vel_elems() * sizeof(double2), cudaMemcpyHostToDevice,
+                               ctx->eng->stream()));
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_vel_download(lddmm_ctx* ctx, const double* dv, double* hv) {
+  return guard(ctx, [&] {
+    LDDMM_CUDA(cudaMemcpyAsync(hv, dv, ctx->eng->vel_elems() * sizeof(double2), cudaMemcpyDeviceToHost,
+                               ctx->eng->stream()));
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_vel_axpy(lddmm_ctx* ctx, double a, const double* x, const double* y, double* out) {
+  return guard(ctx, [&] { ctx->eng->tv_axpy(a, D2(x), D2(y), D2(out)); });
+}
+int lddmm_vel_scale(lddmm_ctx* ctx, const double* x, double a, double* out) {
+  return guard(ctx, [&] { ctx->eng->tv_scaled(D2(x), a, D2(out)); });
+}
+int lddmm_vel_inner(lddmm_ctx* ctx, const double* x, const double* y, double* out) {
+  return guard(ctx, [&] { *out = ctx->eng->tv_inner(D2(x), D2(y)); });
+}
+int lddmm_vel_linf(lddmm_ctx* ctx, const double* x, double* out) {
+  return guard(ctx, [&] { *out = ctx->eng->tv_linf(D2(x)); });
+}
+int lddmm_vel_all_finite(lddmm_ctx* ctx, const double* x, int* out) {
+  return guard(ctx, [&] { *out = ctx->eng->tv_all_finite(D2(x)) ? 1 : 0; });
+}
+
+int lddmm_forward(lddmm_ctx* ctx, const double* v, int with_adjoint, lddmm_energies* out, int* step) {
+  return guard(
+      ctx,
+      [&] {
+        Energies e = ctx->eng->forward(D2(v), with_adjoint != 0);
+        if (out) *out = lddmm_energies{e.energy, e.energy_reg, e.energy_data, e.cfl};
+      },
+      step);
+}
+
+int lddmm_energy(lddmm_ctx* ctx, const double* v, double* energy, int* step) {
+  return guard(ctx, [&] { *energy = ctx->eng->energy(D2(v)); }, step);
+}
+
+int lddmm_gradient(lddmm_ctx* ctx, double* out) {
+  return guard(ctx, [&] {
+    ctx->eng->gradient(D2(out));
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_hessvec(lddmm_ctx* ctx, const double* dv, double* out, int* step) {
+  return guard(
+      ctx,
+      [&] {
+        ctx->eng->hessvec(D2(dv), D2(out));
+        ctx->eng->sync();
+      },
+      step);
+}
+
+int lddmm_precondition(lddmm_ctx* ctx, const double* in, double* out) {
+  return guard(ctx, [&] {
+    ctx->eng->precondition(D2(in), D2(out));
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_get_fields(lddmm_ctx* ctx, double* m1, double* res) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts();
+    DevBuf<double> tmp(N);
+    if (m1) {
+      launch_f32_to_f64(N, e.m1(), tmp.p, e.stream());
+      LDDMM_CUDA(cudaMemcpyAsync(m1, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+      e.sync();
+    }
+    if (res) {
+      launch_f32_to_f64(N, e.residual(), tmp.p, e.stream());
+      LDDMM_CUDA(cudaMemcpyAsync(res, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+      e.sync();
+    }
+  });
+}
+
+int lddmm_get_grid(lddmm_ctx* ctx, int which, double* host_out) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts();
+    const float* src = e.grid_field(which);
+    shape_require(src != nullptr, "lddmm_get_grid: unknown field");
+    DevBuf<double> tmp(N);
+    launch_f32_to_f64(N, src, tmp.p, e.stream());
+    LDDMM_CUDA(cudaMemcpyAsync(host_out, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+    e.sync();
+  });
+}
+
+int lddmm_get_series(lddmm_ctx* ctx, int which, double* host_out) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long n = (e.problem().nt + 1) * e.vec_elems();
+    DevBuf<double2> tmp(n);
+    e.series(which, tmp.p);
+    LDDMM_CUDA(cudaMemcpy(host_out, tmp.p, n * sizeof(double2), cudaMemcpyDeviceToHost));
+  });
+}
+
+int lddmm_optimize(lddmm_ctx* ctx, double* v, const lddmm_options* opt, lddmm_iteration_record* hist, int cap,
+                   lddmm_result* res) {
+  return guard(ctx, [&] {
+    OptimizeResult r = optimize(*ctx->eng, D2(v), to_opts(opt));
+    ctx->eng->sync();
+    fill_result(r, hist, cap, res);
+  });
+}
+
+int lddmm_register(lddmm_ctx* ctx, const double* I0, const double* I1, const lddmm_options* opt, double* host_v,
+                   lddmm_iteration_record* hist, int cap, lddmm_result* res) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    e.set_images_host(I0, I1);
+    DevBuf<double2> v(e.vel_elems());
+    LDDMM_CUDA(cudaMemsetAsync(v.p, 0, e.vel_elems() * sizeof(double2), e.stream()));
+    OptimizeResult r = optimize(e, v.p, to_opts(opt));
+    if (host_v)
+      LDDMM_CUDA(cudaMemcpyAsync(host_v, v.p, e.vel_elems() * sizeof(double2), cudaMemcpyDeviceToHost, e.stream()));
+    e.sync();
+    fill_result(r, hist, cap, res);
+  });
+}
+
+int lddmm_maps(lddmm_ctx* ctx, const double* v, double* hf, double* hi, double jac[4]) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts();
+    DevBuf<float> f(3 * N), i(3 * N);
+    e.maps(D2(v), f.p, i.p, jac);
+    DevBuf<double> t(3 * N);
+    if (hf) {
+      launch_f32_to_f64(3 * N, f.p, t.p, e.stream());
+      LDDMM_CUDA(cudaMemcpyAsync(hf, t.p, 3 * N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+      e.sync();
+    }
+    if (hi) {
+      launch_f32_to_f64(3 * N, i.p, t.p, e.stream());
+      LDDMM_CUDA(cudaMemcpyAsync(hi, t.p, 3 * N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+      e.sync();
+    }
+  });
+}
+
+int lddmm_op_embed(lddmm_ctx* ctx, const double* band, int ncomp, float* grid, int prefilter) {
+  return guard(ctx, [&] {
+    ctx->eng->embed(D2(band), ncomp, grid, prefilter != 0);
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_op_project(lddmm_ctx* ctx, const float* grid, int ncomp, double* band) {
+  return guard(ctx, [&] {
+    ctx->eng->project(grid, ncomp, D2(band));
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_op_advect(lddmm_ctx* ctx, const double* band, int ncomp, const float* dep, double* out) {
+  return guard(ctx, [&] {
+    ctx->eng->advect(D2(band), ncomp, dep, D2(out));
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_op_departure(lddmm_ctx* ctx, const double* v, float* df, float* db, double* cfl) {
+  return guard(ctx, [&] { ctx->eng->departure(D2(v), df, db, cfl); });
+}
+
+int lddmm_op_band(lddmm_ctx* ctx, int op, const double* a, const double* b, double* out) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    switch (op) {
+      case 0: e.star_ss(D2(a), D2(b), D2(out), 1.0); break;
+      case 1: e.star_sv(D2(a), D2(b), D2(out), 1.0); break;
+      case 2: e.star_dot(D2(a), D2(b), D2(out), 1.0); break;
+      case 3: e.jac_mul(D2(a), D2(b), D2(out), 1.0, false); break;
+      case 4: e.jac_mul(D2(a), D2(b), D2(out), 1.0, true); break;
+      case 5: e.band_divergence(D2(a), D2(out)); break;
+      default: throw EngineError(1, "lddmm_op_band: unknown op");
+    }
+    e.sync();
+  });
+}
+
+int lddmm_op_warp(lddmm_ctx* ctx, const float* field, int ncomp, const float* disp, float* out) {
+  return guard(ctx, [&] {
+    ctx->eng->warp_grid(field, ncomp, disp, out);
+    ctx->eng->sync();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+// Device-resident band-limited SL-LDDMM model (the reference's Model<BandAlgebra>
+// with the semi-Lagrangian integrator, variants.hpp:229-548) for one
+// registration on one B200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace lddmm_b200 {
+
+struct Problem {
+  int dims[3];
+  double spacing[3];
+  int band[3];
+  int nt = 5;
+  int variant = 2;     // 0 original, 1 state_equation, 2 deformation_state_equation (variants.hpp:34)
+  int stationary = 1;  // Parameterization (core.hpp:271)
+  double alpha = 0.0025;
+  int s = 2;
+  double sigma2 = 1.0;
+};
+
+struct Energies {
+  double energy = 0, energy_reg = 0, energy_data = 0, cfl = 0;
+};
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) LDDMM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  T* get() const { return p; }
+  operator T*() const { return p; }
+};
+
+// Provider state for one velocity (VelocityProvider, transport.hpp:109-218),
+// stationary: one slot.
+struct ProviderState {
+  DevBuf<double2> v;     // band velocity copy [3][Kprod]
+  DevBuf<double2> div;   // band divergence [Kprod]
+  DevBuf<float> dep_fwd; // departure displacement, grid units [3][N]
+  DevBuf<float> dep_bwd;
+  double cfl = 0;
+  bool has_bwd = false;
+};
+
+class Engine {
+ public:
+  Engine(const Problem& p, int device);
+  ~Engine();
+
+  const Problem& problem() const { return prob_; }
+  int nodes() const { return prob_.stationary ? 1 : prob_.nt + 1; }
+  long long kprod() const { return full_.kprod(); }
+  long long npts() const { return full_.npts(); }
+  long long vec_elems() const { return 3 * kprod(); }          // one band vector (double2 count)
+  long long vel_elems() const { return nodes() * vec_elems(); }  // one velocity
+  cudaStream_t stream() const { return stream_; }
+  int device() const { return device_; }
+  const int* small_dims() const { return small_.N; }
+
+  // images (reference ScalarField layout, fp64 host or fp32 device)
+  void set_images_host(const double* I0, const double* I1);
+  void set_images_device_f32(const float* I0, const float* I1);
+
+  // ---- Model API (variants.hpp:262-353) ----
+  Energies forward(const double2* v, bool with_adjoint);
+  double energy(const double2* v);  // forward(v, false).energy on a separate trial state
+  void gradient(double2* out);
+  void hessvec(const double2* dv, double2* out);
+  void precondition(const double2* in, double2* out);
+  double reg_energy(const double2* v);
+  const float* m1() const { return m1_.p; }
+  const float* residual() const { return res_.p; }
+  // cached grid fields: 0 m1, 1 residual, 2-4 grad_src_warped, 5 I0 spline coefficients,
+  // 6-8 grad I0 spline coefficients, 9 I1
+  const float* grid_field(int which) const {
+    const long long N = npts();
+    if (which == 0) return m1_.p;
+    if (which == 1) return res_.p;
+    if (which >= 2 && which <= 4) return m1_.p + (which - 1) * N;
+    if (which >= 5 && which <= 8) return I0coef_.p + (which - 5) * N;
+    if (which == 9) return I1_.p;
+    return nullptr;
+  }
+  double residual_sumsq();
+  double mse_denominator();  // l2_inner(I0 - I1, I0 - I1)
+
+  // ---- TimeVaryingVelocity algebra (variants.hpp:65-117) ----
+  void tv_axpy(double a, const double2* x, const double2* y, double2* out);
+  void tv_scaled(const double2* x, double a, double2* out);
+  double tv_inner(const double2* a, const double2* b);
+  double tv_linf(const double2* a);
+  bool tv_all_finite(const double2* a);
+
+  // ---- primitives (parity tests / tools) ----
+  void embed(const double2* c, int ncomp, float* out, bool prefilter = false);  // full grid
+  void project(const float* f, int ncomp, double2* out);
+  void advect(const double2* q, int ncomp, const float* dep, double2* out);
+  void departure(const double2* v, float* dep_fwd, float* dep_bwd, double* cfl);
+  void star_sv(const double2* s, const double2* x, double2* out, double alpha);
+  void star_ss(const double2* a, const double2* b, double2* out, double alpha);
+  void star_dot(const double2* a, const double2* b, double2* out, double alpha);
+  void jac_mul(const double2* u, const double2* w, double2* out, double alpha, bool transpose);
+  void band_divergence(const double2* v, double2* out);
+  // cubic pull-back of grid fields (ncomp <= 6) through x - disp_phys (warp, interp.hpp:178-210)
+  void warp_grid(const float* f, int ncomp, const float* disp_phys, float* out);
+  // endpoint maps and Jacobian ranges (metrics.hpp:24-65); disp outputs optional (device, [3][N] fp32)
+  void maps(const double2* v, float* disp_fwd, float* disp_inv, double jac[4]);
+  void series(int which, double2* out);  // 0 u, 1 rho (nt+1 band vectors)
+
+  // counters (kernel launches issued by this engine)
+  long long launches() const { return launches_; }
+  void sync();
+
+ private:
+  Problem prob_;
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  long long launches_ = 0;
+  double h_[3];
+  double cell_volume_ = 1;
+  double small_ratio_ = 1;  // M / N (total points) for the small product grid
+
+  DftPlan full_, small_;
+  std::vector<void*> plan_allocs_;
+
+  // images
+  DevBuf<float> I1_, I0coef_, gI0coef_;  // I0 spline coefficients, grad I0 spline coefficients [3][N]
+  DevBuf<float> I0f_;                    // I0 values (fp32) for mse denominators
+  double mse_denom_ = -1;
+
+  // scratch: full-grid DFT
+  int fmax_full_ = 6, fmax_small_ = 12;
+  DevBuf<float2> D_, E1_, E2_, G1_, G2_, G3_;
+  DevBuf<float> gridA_, gridB_;  // [fmax][N]
+  // scratch: small grid
+  DevBuf<float2> sD_, sE1_, sE2_, sG1_, sG2_, sG3_;
+  DevBuf<float> sgrid_, sacc_;  // [12][M], [3][M]
+
+  // reductions
+  DevBuf<double> part_, part2_, slots_;
+  double* host_slots_ = nullptr;
+
+  // forward cache (variants.hpp:188-224, deformation variant fields)
+  ProviderState prov_, trial_prov_;
+  bool have_cache_ = false, cache_adjoint_ = false;
+  Energies cache_e_;
+  DevBuf<double2> u_, rho_;   // (nt+1) x 3 x Kprod
+  DevBuf<double2> tmp_u_;     // trial u running state [2][3][Kprod]
+  DevBuf<float> m1_, res_, gsw_, ugrid_;  // m1, residual [N], grad_src_warped [3][N], u(1) embed [3][N]
+  DevBuf<float> trial_m1_, trial_res_;
+  DevBuf<double2> btmp_;      // band temporaries: 12 band vectors
+  DevBuf<double2> src_;       // (nt+1) band vectors (incremental sources)
+  DevBuf<double2> dseries_;   // (nt+1) band vectors (hessvec du / drho series)
+
+  void build_plan(DftPlan& p, const int* Ngrid, const int* K, const double* parent_wunit);
+  void free_plans();
+  double2* bt(int i) const { return btmp_.p + (long long)i * vec_elems(); }
+  double2* node(DevBuf<double2>& s, int i) const { return s.p + (long long)i * vec_elems(); }
+
+  void provider_build(const double2* v, ProviderState& ps, bool with_bwd);
+  void solve_displacement_fwd(ProviderState& ps, double2* series, bool keep_all, double2* last);
+  void solve_vector_continuity_bwd(ProviderState& ps, const double2* q1, double2* series);
+  void solve_incremental_displacement(ProviderState& ps, const double2* dv, double2* series);
+  void warp_m1(const double2* u1, float* m1, float* res, bool want_gsw, double* data_sumsq);
+  void assemble_jacT_terms(const double2* series_u, const double2* series_q, const double2* like,
+                           double2* out);
+  void check_series_finite(const double2* series, int count, int first_step_offset, bool backward);
+  void enqueue_finite_check(const double2* node, int step);
+  void finish_finite_checks(int nsteps);
+  void set_images_impl(const double* I0d);
+
+  // generic pipelines
+  void embed_fields(const DftPlan& p, const PrepArgs& a, float* out, float2* D, float2* E1, float2* E2);
+  void project_fields(const DftPlan& p, const float* f, const FinArgs& a, float2* G1, float2* G2, float2* G3);
+  void advect_multi(const double2* const* in, int nf, const float* dep, const FinField* outs);
+  void small_product(int op, const double2* a, const double2* b, double2* out, double alpha,
+                     const double2* add, double beta);
+
+  double reduce(int nparts, int op);
+  void count(int n = 1) { launches_ += n; }
+};
+
+}  // namespace lddmm_b200

@@ -1,0 +1,307 @@
+// Band-limited projection / embedding as separable truncated DFTs (sm_100a).
+//
+// Replaces spectral.hpp:242-285 (project/embed through a full-grid C2C FFT,
+// fft.hpp:69-101).  A band field holds the centred truncation of the unscaled
+// forward DFT (K_a modes per axis, DFT order, band-Nyquist planes zero,
+// spectral.hpp:8-12).  Because every embedded field is real, only the half
+// band kz in [0, Kz/2) along the fastest axis is carried:
+//
+//   embed   C[kx,ky,kz] --prep--> D[kx,ky,kz<H]           (fold + symbol, fp64->fp32)
+//           --Y--> E1[kx,y,kz] --X--> E2[x,y,kz] --Z--> f[x,y,z]   (real output, /N)
+//   project f[x,y,z] --Z--> G1[x,y,kz] --X--> G2[kx,y,kz] --Y--> G3[kx,ky,kz]
+//           --finalize--> C[kx,ky,kz]  (Hermitian completion kz<0, Nyquist zero, fp64)
+//
+// The fold D = C(k) + conj(C(-k)) for kz > 0 makes Re(sum over the half band)
+// identical to the reference's Re(full complex inverse DFT) for ANY coefficient
+// set, including ones that are only Hermitian to round-off.  Symbols that are
+// Hermitian (i*omega derivatives, the B-spline prefilter 1/B(k), real scales)
+// commute with the fold and are applied in the prep step.
+//
+// X/Y stages are batched complex GEMMs against fp32 twiddle tables generated in
+// fp64; the Z stages are real GEMMs (K = Kz for embed, K = Nz for project).
+// All products accumulate in fp32.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace lddmm_b200 {
+
+// ---------------------------------------------------------------------------
+// prep: fp64 band -> fp32 half band with fold and symbol
+
+__global__ void band_prep_kernel(PrepArgs a, int Kx, int Ky, int Kz, int Nx, int Ny, int Nz, double wx,
+                                 double wy, double wz, float2* __restrict__ D) {
+  const int H = Kz / 2;
+  const long long per = (long long)Kx * Ky * H;
+  const long long total = per * a.nf;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(t / per);
+    long long r = t - (long long)f * per;
+    const int fz = (int)(r % H);
+    r /= H;
+    const int fy = (int)(r % Ky);
+    const int fx = (int)(r / Ky);
+    float2 out = make_float2(0.f, 0.f);
+    const PrepField pf = a.f[f];
+    if (fx != Kx / 2 && fy != Ky / 2 && pf.src != nullptr) {
+      const double2* C = pf.src;
+      double2 v = C[((long long)fx * Ky + fy) * Kz + fz];
+      if (fz > 0) {
+        const int mx = (Kx - fx) % Kx, my = (Ky - fy) % Ky, mz = Kz - fz;
+        const double2 w = C[((long long)mx * Ky + my) * Kz + mz];
+        v.x += w.x;
+        v.y -= w.y;
+      }
+      const int kx = fx < Kx / 2 ? fx : fx - Kx;
+      const int ky = fy < Ky / 2 ? fy : fy - Ky;
+      const int kz = fz;
+      double s = pf.scale;
+      if (pf.sym & SYM_PREFILTER) {
+        // 1 / B(k), B(k) = prod_a (4 + 2 cos(2 pi k_a / N_a)) / 6 (exact periodic cubic
+        // B-spline prefilter of interp.hpp:23-63 in Fourier form)
+        const double bx = (4.0 + 2.0 * cospi(2.0 * kx / Nx)) / 6.0;
+        const double by = (4.0 + 2.0 * cospi(2.0 * ky / Ny)) / 6.0;
+        const double bz = (4.0 + 2.0 * cospi(2.0 * kz / Nz)) / 6.0;
+        s /= (bx * by * bz);
+      }
+      const int dax = pf.sym & SYM_DERIV_MASK;
+      if (dax) {
+        // band_derivative: multiply by i*omega_a, omega = 2 pi k / (N_a h_a) (spectral.hpp:77-79,419-427)
+        const double om = dax == 1 ? wx * kx : (dax == 2 ? wy * ky : wz * kz);
+        const double re = -v.y * om, im = v.x * om;
+        v.x = re;
+        v.y = im;
+      }
+      out = make_float2((float)(v.x * s), (float)(v.y * s));
+    }
+    D[t] = out;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// finalize: G3 half band (fp32) -> full band fp64 with Hermitian completion
+
+__global__ void band_finalize_kernel(FinArgs a, int Kx, int Ky, int Kz, const float2* __restrict__ G) {
+  const int H = Kz / 2;
+  const long long per = (long long)Kx * Ky * Kz;
+  const long long total = per * a.nf;
+  const long long gper = (long long)Kx * Ky * H;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(t / per);
+    long long r = t - (long long)f * per;
+    const int fz = (int)(r % Kz);
+    r /= Kz;
+    const int fy = (int)(r % Ky);
+    const int fx = (int)(r / Ky);
+    double gx = 0.0, gy = 0.0;
+    if (fx != Kx / 2 && fy != Ky / 2 && fz != H) {
+      const float2* Gf = G + (long long)f * gper;
+      if (fz < H) {
+        const float2 g = Gf[((long long)fx * Ky + fy) * H + fz];
+        gx = g.x;
+        gy = g.y;
+      } else {
+        const int mx = (Kx - fx) % Kx, my = (Ky - fy) % Ky, mz = Kz - fz;
+        const float2 g = Gf[((long long)mx * Ky + my) * H + mz];
+        gx = g.x;
+        gy = -g.y;
+      }
+    }
+    const FinField ff = a.f[f];
+    const long long idx = r * Kz + fz;  // (fx*Ky+fy)*Kz+fz
+    double2 o = make_double2(ff.alpha * gx, ff.alpha * gy);
+    if (ff.add) {
+      const double2 ad = ff.add[idx];
+      o.x += ff.beta * ad.x;
+      o.y += ff.beta * ad.y;
+    }
+    ff.dst[idx] = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// batched complex GEMM: C[b][m][n] = sum_k A[m][k] * B[b][k][n]
+// 32x32 tile, 256 threads, 2x2 complex outputs per thread, BK = 16.
+
+constexpr int CG_BM = 32, CG_BN = 32, CG_BK = 16;
+
+__global__ __launch_bounds__(256) void cgemm_kernel(const float2* __restrict__ A, int lda,
+                                                    const float2* __restrict__ B, long long sB, int ldb,
+                                                    float2* __restrict__ C, long long sC, int ldc, int M,
+                                                    int N, int K) {
+  __shared__ float2 As[CG_BK][CG_BM + 1];
+  __shared__ float2 Bs[CG_BK][CG_BN + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * CG_BM, n0 = blockIdx.x * CG_BN;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+  float2 acc[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  for (int k0 = 0; k0 < K; k0 += CG_BK) {
+    for (int e = tid; e < CG_BM * CG_BK; e += 256) {
+      const int mm = e / CG_BK, kk = e % CG_BK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? A[(long long)gm * lda + gk] : make_float2(0.f, 0.f);
+    }
+    for (int e = tid; e < CG_BK * CG_BN; e += 256) {
+      const int kk = e / CG_BN, nn = e % CG_BN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      Bs[kk][nn] = (gk < K && gn < N) ? B[(long long)gk * ldb + gn] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < CG_BK; ++kk) {
+      const float2 a0 = As[kk][ty], a1 = As[kk][ty + 16];
+      const float2 b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
+      acc[0][0].x = fmaf(a0.x, b0.x, fmaf(-a0.y, b0.y, acc[0][0].x));
+      acc[0][0].y = fmaf(a0.x, b0.y, fmaf(a0.y, b0.x, acc[0][0].y));
+      acc[0][1].x = fmaf(a0.x, b1.x, fmaf(-a0.y, b1.y, acc[0][1].x));
+      acc[0][1].y = fmaf(a0.x, b1.y, fmaf(a0.y, b1.x, acc[0][1].y));
+      acc[1][0].x = fmaf(a1.x, b0.x, fmaf(-a1.y, b0.y, acc[1][0].x));
+      acc[1][0].y = fmaf(a1.x, b0.y, fmaf(a1.y, b0.x, acc[1][0].y));
+      acc[1][1].x = fmaf(a1.x, b1.x, fmaf(-a1.y, b1.y, acc[1][1].x));
+      acc[1][1].y = fmaf(a1.x, b1.y, fmaf(a1.y, b1.x, acc[1][1].y));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+      if (gm < M && gn < N) C[(long long)gm * ldc + gn] = acc[i][j];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// batched real GEMM for the Z stages: C[b][m][n] = sum_k A[b][m][k] * B[k][n]
+// BM = 128, BK = 16, thread tile 8 x 4.  BN = 64 (256 threads) or 32 (128 threads).
+
+template <int BN>
+__global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__ A, int lda, long long sA,
+                                                       const float* __restrict__ B, int ldb,
+                                                       float* __restrict__ C, int ldc, long long sC, int M,
+                                                       int N, int K) {
+  constexpr int BM = 128, BK = 16, NT = BN * 4, TXN = BN / 4;
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % TXN, ty = tid / TXN;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  A += blockIdx.z * sA;
+  C += blockIdx.z * sC;
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll 4
+    for (int e = tid; e < BM * BK; e += NT) {
+      const int mm = e / BK, kk = e % BK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? __ldg(A + (long long)gm * lda + gk) : 0.f;
+    }
+#pragma unroll 4
+    for (int e = tid; e < BK * BN; e += NT) {
+      const int kk = e / BN, nn = e % BN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      Bs[kk][nn] = (gk < K && gn < N) ? __ldg(B + (long long)gk * ldb + gn) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const int gn = n0 + tx * 4;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int gm = m0 + ty * 8 + i;
+    if (gm >= M) break;
+    float* crow = C + (long long)gm * ldc;
+    if (gn + 3 < N && (ldc & 3) == 0) {
+      *reinterpret_cast<float4*>(crow + gn) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (gn + j < N) crow[gn + j] = acc[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+void launch_band_prep(const PrepArgs& a, const DftPlan& p, float2* D, cudaStream_t s) {
+  const long long total = (long long)p.K[0] * p.K[1] * (p.K[2] / 2) * a.nf;
+  band_prep_kernel<<<grid_for(total, 256), 256, 0, s>>>(a, p.K[0], p.K[1], p.K[2], p.N[0], p.N[1], p.N[2],
+                                                        p.omega_unit[0], p.omega_unit[1], p.omega_unit[2], D);
+  LDDMM_LAUNCH_CHECK();
+}
+
+void launch_band_finalize(const FinArgs& a, const DftPlan& p, const float2* G, cudaStream_t s) {
+  const long long total = (long long)p.K[0] * p.K[1] * p.K[2] * a.nf;
+  band_finalize_kernel<<<grid_for(total, 256), 256, 0, s>>>(a, p.K[0], p.K[1], p.K[2], G);
+  LDDMM_LAUNCH_CHECK();
+}
+
+void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int ldb, float2* C, long long sC,
+                  int ldc, int M, int N, int K, int batch, cudaStream_t s) {
+  dim3 grid(ceil_div(N, CG_BN), ceil_div(M, CG_BM), batch);
+  cgemm_kernel<<<grid, 256, 0, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K);
+  LDDMM_LAUNCH_CHECK();
+}
+
+void launch_sgemm(const float* A, int lda, long long sA, const float* B, int ldb, float* C, int ldc,
+                  long long sC, int M, int N, int K, int batch, cudaStream_t s) {
+  if (N <= 32) {
+    dim3 grid(ceil_div(N, 32), ceil_div(M, 128), batch);
+    sgemm_kernel<32><<<grid, 128, 0, s>>>(A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
+  } else {
+    dim3 grid(ceil_div(N, 64), ceil_div(M, 128), batch);
+    sgemm_kernel<64><<<grid, 256, 0, s>>>(A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
+  }
+  LDDMM_LAUNCH_CHECK();
+}
+
+// embed nf half-band fields D[nf][Kx][Ky][H] -> grid fields out[nf][N] (fp32)
+void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2, float* out, cudaStream_t s) {
+  const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
+  const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
+  // Y: for each (f,kx): E1[Ny x H] = Wy[Ny x Ky] * D[Ky x H]
+  launch_cgemm(p.wy_e, Ky, D, (long long)Ky * H, H, E1, (long long)Ny * H, H, Ny, H, Ky, nf * Kx, s);
+  // X: for each f: E2[Nx x (Ny H)] = Wx[Nx x Kx] * E1[Kx x (Ny H)]
+  launch_cgemm(p.wx_e, Kx, E1, (long long)Kx * Ny * H, Ny * H, E2, (long long)Nx * Ny * H, Ny * H, Nx, Ny * H,
+               Kx, nf, s);
+  // Z: for each f: out[(Nx Ny) x Nz] = E2 as float[(Nx Ny) x 2H] * Tz_e[2H x Nz]
+  launch_sgemm(reinterpret_cast<const float*>(E2), 2 * H, (long long)Nx * Ny * 2 * H, p.tz_e, Nz, out, Nz,
+               (long long)Nx * Ny * Nz, Nx * Ny, Nz, 2 * H, nf, s);
+}
+
+// project nf grid fields f[nf][N] -> half band G3[nf][Kx][Ky][H]
+void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, float2* G3, cudaStream_t s) {
+  const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
+  const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
+  launch_sgemm(f, Nz, (long long)Nx * Ny * Nz, p.tz_p, 2 * H, reinterpret_cast<float*>(G1), 2 * H,
+               (long long)Nx * Ny * 2 * H, Nx * Ny, 2 * H, Nz, nf, s);
+  launch_cgemm(p.wx_p, Nx, G1, (long long)Nx * Ny * H, Ny * H, G2, (long long)Kx * Ny * H, Ny * H, Kx, Ny * H,
+               Nx, nf, s);
+  launch_cgemm(p.wy_p, Ny, G2, (long long)Ny * H, H, G3, (long long)Ky * H, H, Ky, H, Ny, nf * Kx, s);
+}
+
+}  // namespace lddmm_b200
