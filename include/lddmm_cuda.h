@@ -108,6 +108,13 @@ void lddmm_destroy(lddmm_ctx* ctx);
 const char* lddmm_last_error(const lddmm_ctx* ctx);
 int lddmm_sync(lddmm_ctx* ctx);
 long long lddmm_launch_count(void); /* kernels launched by this library (process-wide) */
+/* the context's CUDA stream (cudaStream_t), for events / external synchronisation */
+void* lddmm_stream(lddmm_ctx* ctx);
+/* live SL-gather timing: CUDA events around every gather launch while on;
+ * stats = device ms summed over launches, launch count, algorithmic bytes
+ * sum of N * (12 + 8 C) */
+int lddmm_gather_timing(lddmm_ctx* ctx, int on);
+int lddmm_gather_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* bytes);
 
 /* Model::source / Model::target (variants.hpp:238-239): host fp64 ScalarFields */
 int lddmm_set_images(lddmm_ctx* ctx, const double* host_I0, const double* host_I1);

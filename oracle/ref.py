@@ -350,6 +350,52 @@ def jacobian_determinant(disp, dims, spacing):
     return ob
 
 
+# ---- timing of the reference's own primitives (bench cpu_baseline) -------------------
+
+def time_ops(dims, spacing, band, mask=0b0111):
+    """Milliseconds of one reference FFT / prefilter / cubic gather / vector advect at `dims`."""
+    d, di, hi = _grid_args(dims, spacing)
+    t = np.full(4, np.nan)
+    tb, tp = _d(t)
+    _check(lib().ref_time_ops(d, di, hi, _i(band), int(mask), tp), "time_ops")
+    return dict(fft=tb[0], prefilter=tb[1], gather=tb[2], advect=tb[3])
+
+
+def defstate_op_counts_measured(nt, forwards, hessvecs, trials):
+    """As defstate_op_counts, for a run that did `forwards` adjoint forwards (+ gradients),
+    `hessvecs` Hessian-vector products and `trials` energy-only line-search trials."""
+    nt_ = nt
+    fwd_adj = dict(fft=38 * nt_ + 13, warp=12 * nt_ + 4, pre=3, gath=6)
+    energy = dict(fft=12 * nt_ + 6, warp=6 * nt_ + 1, pre=3, gath=3)
+    grad = dict(fft=15 * (nt_ + 1), warp=0, pre=0, gath=0)
+    hv = dict(fft=83 * nt_ + 21, warp=12 * nt_, pre=0, gath=0)
+    return {k: forwards * (fwd_adj[k] + grad[k]) + hessvecs * hv[k] + trials * energy[k] for k in fwd_adj}
+
+
+def defstate_op_counts(nt, gn_iters, pcg_per_iter, trials_per_iter=1):
+    """Full-grid transform / warp counts of one reference registration (deformation-state
+    variant, SL, stationary, band-limited), read off the reference code paths:
+      forward+adjoint 38nt+13 FFTs (variants.hpp:424-433, transport.hpp:264-298),
+      energy-only 12nt+6, gradient 15(nt+1) (band_jacT_mul: 3+9 embeds, 3 projects),
+      hessvec 83nt+21 (variants.hpp:313-344); scalar cubic warps (prefilter + gather):
+      forward+adjoint 12nt+4, energy 6nt+1, hessvec 12nt; plus the provider's sampler
+      prefilters (3) and departure gathers (3 per direction)."""
+    fwd_adj = dict(fft=38 * nt + 13, warp=12 * nt + 4, pre=3, gath=6)
+    energy = dict(fft=12 * nt + 6, warp=6 * nt + 1, pre=3, gath=3)
+    grad = dict(fft=15 * (nt + 1), warp=0, pre=0, gath=0)
+    hv = dict(fft=83 * nt + 21, warp=12 * nt, pre=0, gath=0)
+    tot = {k: fwd_adj[k] + grad[k] for k in fwd_adj}
+    for _ in range(gn_iters):
+        for k in tot:
+            tot[k] += pcg_per_iter * hv[k] + trials_per_iter * energy[k] + fwd_adj[k] + grad[k]
+    return tot
+
+
+def registration_cost_ms(times, counts):
+    return (counts["fft"] * times["fft"] + counts["warp"] * (times["prefilter"] + times["gather"])
+            + counts["pre"] * times["prefilter"] + counts["gath"] * times["gather"])
+
+
 # ---- synth.hpp / io.hpp -------------------------------------------------------------
 
 def blob_pair(dims, spacing, seed):

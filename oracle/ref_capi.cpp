@@ -377,6 +377,59 @@ int ref_jacobian_determinant(int d, const int* dims, const double* h, const doub
   });
 }
 
+// ---- timing of the reference's own primitives (bench.py cpu_baseline) ---------------
+// times[0] one full-grid complex DFT (fft_forward, fft.hpp:69-73)
+// times[1] one scalar spline prefilter (spline_coefficients, interp.hpp:80-84)
+// times[2] one scalar cubic gather at N points with a prebuilt sampler (warp, interp.hpp:191-200)
+// times[3] one vector advect_state of a band field (transport.hpp:71-73), end to end
+// mask selects which to run (bit i -> times[i]); unselected entries are left untouched.
+int ref_time_ops(int d, const int* dims, const double* h, const int* band, int mask, double* times) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    auto ms = [](clk::time_point a) {
+      return std::chrono::duration<double, std::milli>(clk::now() - a).count();
+    };
+    GridSpec g = make_grid(d, dims, h);
+    BandSpec b = make_band(g, band);
+    // smooth field and departure-like points x - 0.3 sin(.)
+    ScalarField f(g);
+    std::array<int, kMaxDim> idx{};
+    for (std::size_t i = 0; i < g.size(); ++i) {
+      g.unflatten(i, idx);
+      double s = 0.0;
+      for (int a = 0; a < g.d; ++a) s += std::sin(2.0 * M_PI * idx[a] / g.dims[a]);
+      f.v[i] = s;
+    }
+    VectorField pts = identity_map(g);
+    for (int a = 0; a < g.d; ++a)
+      for (std::size_t i = 0; i < g.size(); ++i) pts.comp[a][i] -= 0.3 * std::sin(0.01 * (double)i + a);
+    if (mask & 1) {
+      std::vector<cplx> buf = fft_of(f);  // plan created here (not timed)
+      auto t0 = clk::now();
+      fft_forward(g, buf.data());
+      times[0] = ms(t0);
+    }
+    if (mask & 2) {
+      auto t0 = clk::now();
+      ScalarField c = spline_coefficients(f);
+      times[1] = ms(t0);
+    }
+    if (mask & 4) {
+      ScalarSampler s(f, Interp::cubic);
+      auto t0 = clk::now();
+      ScalarField r = warp(s, pts);
+      times[2] = ms(t0);
+    }
+    if (mask & 8) {
+      BandVectorField q(b);
+      for (int a = 0; a < g.d; ++a) q.comp[a] = project(f, b).c;
+      auto t0 = clk::now();
+      BandVectorField r = advect_state(q, pts);
+      times[3] = ms(t0);
+    }
+  });
+}
+
 // ---- synth.hpp / io.hpp ---------------------------------------------------------
 int ref_blob_pair(int d, const int* dims, const double* h, unsigned long long seed, double* src, double* tgt) {
   return guard([&] {

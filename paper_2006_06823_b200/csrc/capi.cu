@@ -139,6 +139,16 @@ int lddmm_sync(lddmm_ctx* ctx) {
 
 long long lddmm_launch_count(void) { return launch_counter(); }
 
+void* lddmm_stream(lddmm_ctx* ctx) { return (void*)ctx->eng->stream(); }
+
+int lddmm_gather_timing(lddmm_ctx* ctx, int on) {
+  return guard(ctx, [&] { ctx->eng->set_gather_timing(on != 0); });
+}
+
+int lddmm_gather_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* bytes) {
+  return guard(ctx, [&] { ctx->eng->gather_stats(ms, launches, bytes); });
+}
+
 int lddmm_set_images(lddmm_ctx* ctx, const double* I0, const double* I1) {
   return guard(ctx, [&] { ctx->eng->set_images_host(I0, I1); });
 }

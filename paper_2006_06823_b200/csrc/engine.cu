@@ -117,9 +117,16 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   I1_.alloc(N);
   I0f_.alloc(N);
   I0coef_.alloc(4 * N);  // I0 spline coefficients followed by grad I0 spline coefficients
+  f64a_.alloc(N);
+  f64b_.alloc(N);
+  f64c_.alloc(N);
+  dker_.alloc(3 * 1024);
+  shape_require(p.dims[0] <= 1024 && p.dims[1] <= 1024 && p.dims[2] <= 1024, "grid dims must be <= 1024");
+  opt_ws_.alloc(9 * vel_elems());
 }
 
 Engine::~Engine() {
+  for (cudaEvent_t e : gt_events_) cudaEventDestroy(e);
   free_plans();
   if (host_slots_) cudaFreeHost(host_slots_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -183,6 +190,43 @@ void Engine::build_plan(DftPlan& p, const int* Ng, const int* K, const double* w
   p.tz_p = (float*)upload(tz_p.data(), tz_p.size() * sizeof(float));
 }
 
+void Engine::timed_gather(const float* coef, int ncomp, const float* dep, float* out) {
+  if (!gt_on_) {
+    launch_gather_cubic(coef, ncomp, dep, out, full_.N, stream_);
+    return;
+  }
+  while (gt_events_.size() < 2 * (gt_used_ + 1)) {
+    cudaEvent_t e;
+    LDDMM_CUDA(cudaEventCreate(&e));
+    gt_events_.push_back(e);
+  }
+  LDDMM_CUDA(cudaEventRecord(gt_events_[2 * gt_used_], stream_));
+  launch_gather_cubic(coef, ncomp, dep, out, full_.N, stream_);
+  LDDMM_CUDA(cudaEventRecord(gt_events_[2 * gt_used_ + 1], stream_));
+  if (gt_bytes_.size() <= gt_used_) gt_bytes_.resize(gt_used_ + 1);
+  gt_bytes_[gt_used_] = (double)npts() * (12.0 + 8.0 * ncomp);
+  ++gt_used_;
+}
+
+void Engine::set_gather_timing(bool on) {
+  gt_on_ = on;
+  gt_used_ = 0;
+}
+
+void Engine::gather_stats(double* ms, long long* launches, double* bytes) {
+  sync();
+  double t = 0.0, b = 0.0;
+  for (size_t i = 0; i < gt_used_; ++i) {
+    float e = 0.f;
+    LDDMM_CUDA(cudaEventElapsedTime(&e, gt_events_[2 * i], gt_events_[2 * i + 1]));
+    t += e;
+    b += gt_bytes_[i];
+  }
+  *ms = t;
+  *launches = (long long)gt_used_;
+  *bytes = b;
+}
+
 double Engine::reduce(int nparts, int op) {
   launch_reduce_final(part_, nparts, op, slots_.p, stream_);
   LDDMM_CUDA(cudaMemcpyAsync(host_slots_, slots_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_));
@@ -196,21 +240,21 @@ double Engine::reduce(int nparts, int op) {
 
 void Engine::set_images_host(const double* I0, const double* I1) {
   const long long N = npts();
-  DevBuf<double> d0(N), d1(N);
-  LDDMM_CUDA(cudaMemcpyAsync(d0.p, I0, N * sizeof(double), cudaMemcpyHostToDevice, stream_));
-  LDDMM_CUDA(cudaMemcpyAsync(d1.p, I1, N * sizeof(double), cudaMemcpyHostToDevice, stream_));
-  launch_f64_to_f32(N, d0.p, I0f_.p, stream_);
-  launch_f64_to_f32(N, d1.p, I1_.p, stream_);
-  set_images_impl(d0.p);
+  double* d0 = f64a_.p;
+  double* d1 = f64b_.p;
+  LDDMM_CUDA(cudaMemcpyAsync(d0, I0, N * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  LDDMM_CUDA(cudaMemcpyAsync(d1, I1, N * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  launch_f64_to_f32(N, d0, I0f_.p, stream_);
+  launch_f64_to_f32(N, d1, I1_.p, stream_);
+  set_images_impl(d0);
 }
 
 void Engine::set_images_device_f32(const float* I0, const float* I1) {
   const long long N = npts();
   LDDMM_CUDA(cudaMemcpyAsync(I1_.p, I1, N * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
   LDDMM_CUDA(cudaMemcpyAsync(I0f_.p, I0, N * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
-  DevBuf<double> d0(N);
-  launch_f32_to_f64(N, I0, d0.p, stream_);
-  set_images_impl(d0.p);
+  launch_f32_to_f64(N, I0, f64a_.p, stream_);
+  set_images_impl(f64a_.p);
 }
 
 // I0 (fp64 on device) -> I0 spline coefficients, grad I0 spline coefficients,
@@ -220,10 +264,10 @@ void Engine::set_images_impl(const double* I0d) {
   const float* I0 = I0f_.p;
   const float* I1 = I1_.p;
   // I0 spline coefficients (fp64 recursion, interp.hpp:80-84)
-  DevBuf<double> c(N);
-  LDDMM_CUDA(cudaMemcpyAsync(c.p, I0d, N * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
-  launch_prefilter3d(c.p, full_.N, stream_);
-  launch_f64_to_f32(N, c.p, I0coef_.p, stream_);
+  double* c = f64c_.p;  // I0d is f64a_
+  LDDMM_CUDA(cudaMemcpyAsync(c, I0d, N * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  launch_prefilter3d(c, full_.N, stream_);
+  launch_f64_to_f32(N, c, I0coef_.p, stream_);
   // spectral_gradient(I0) (spectral.hpp:326-334,356-370) in fp64: per axis a real
   // circulant derivative kernel D_a[d] = (1/n) sum_k i omega_k e^{2 pi i k d / n}
   // (Nyquist k = n/2 excluded, omega = 2 pi k / (n h)), then the spline prefilter.
@@ -239,17 +283,15 @@ void Engine::set_images_impl(const double* I0d) {
       }
       Dh[d] = (double)(acc / n);
     }
-    DevBuf<double> Dd(n), g(N);
-    LDDMM_CUDA(cudaMemcpyAsync(Dd.p, Dh.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream_));
-    launch_circulant_axis_f64(I0d, g.p, Dd.p, a, full_.N, stream_);
-    launch_prefilter3d(g.p, full_.N, stream_);
-    launch_f64_to_f32(N, g.p, I0coef_.p + (a + 1) * N, stream_);
-    sync();
+    double* g = f64b_.p;
+    LDDMM_CUDA(cudaMemcpyAsync(dker_.p + 1024 * a, Dh.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    launch_circulant_axis_f64(I0d, g, dker_.p + 1024 * a, a, full_.N, stream_);
+    launch_prefilter3d(g, full_.N, stream_);
+    launch_f64_to_f32(N, g, I0coef_.p + (a + 1) * N, stream_);
   }
   // mse denominator l2_inner(I0 - I1) (optimizer.hpp:151-154)
   {
-    DevBuf<float> d(N);
-    const int g = launch_residual(N, I0, I1, d.p, part_.p, stream_);
+    const int g = launch_residual(N, I0, I1, gridB_.p, part_.p, stream_);
     mse_denom_ = reduce(g, 0) * cell_volume_;
   }
   have_cache_ = false;
@@ -280,7 +322,7 @@ void Engine::advect_multi(const double2* const* in, int nf, const float* dep, co
     pa.nf = n;
     for (int i = 0; i < n; ++i) pa.f[i] = PrepField{in[c0 + i], SYM_PREFILTER, 1.0};
     embed_fields(full_, pa, gridA_.p, D_.p, E1_.p, E2_.p);
-    launch_gather_cubic(gridA_.p, n, dep, gridB_.p, full_.N, stream_);
+    timed_gather(gridA_.p, n, dep, gridB_.p);
     FinArgs fa{};
     fa.nf = n;
     for (int i = 0; i < n; ++i) fa.f[i] = outs[c0 + i];
@@ -350,11 +392,11 @@ void Engine::warp_grid(const float* f, int ncomp, const float* disp_phys, float*
   const long long N = npts();
   shape_require(ncomp >= 1 && ncomp <= fmax_full_, "warp_grid: 1..6 components");
   LDDMM_CUDA(cudaMemcpyAsync(gridA_.p, f, ncomp * N * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
-  DevBuf<double> c(N);
+  double* c = f64c_.p;
   for (int k = 0; k < ncomp; ++k) {
-    launch_f32_to_f64(N, gridA_.p + k * N, c.p, stream_);
-    launch_prefilter3d(c.p, full_.N, stream_);
-    launch_f64_to_f32(N, c.p, gridA_.p + k * N, stream_);
+    launch_f32_to_f64(N, gridA_.p + k * N, c, stream_);
+    launch_prefilter3d(c, full_.N, stream_);
+    launch_f64_to_f32(N, c, gridA_.p + k * N, stream_);
   }
   for (int k = 0; k < ncomp;) {
     const int n = (ncomp - k >= 4) ? 4 : (ncomp - k >= 3 ? 3 : 1);
@@ -719,7 +761,8 @@ void Engine::maps(const double2* v, float* disp_fwd, float* disp_inv, double jac
     if (dst) embed(d, 3, dst, false);
     // 9 derivative embeds d_b u_a: spectral_derivative of a band-limited field is
     // embed(i omega_b u_a) (its grid-Nyquist content is zero)
-    DevBuf<float> du(9 * N);
+    if (maps_du_.n < (size_t)(9 * N)) maps_du_.alloc(9 * N);
+    DevBuf<float>& du = maps_du_;
     int done = 0;
     while (done < 9) {
       const int n = std::min(fmax_full_, 9 - done);

@@ -131,6 +131,13 @@ class Engine {
   // counters (kernel launches issued by this engine)
   long long launches() const { return launches_; }
   void sync();
+  double2* opt_ws(int i) const { return opt_ws_.p + (long long)i * vel_elems(); }
+
+  // Live per-launch timing of the SL gather kernel (CUDA events on the engine
+  // stream around every gather launch while enabled).  stats: total device ms,
+  // launch count, algorithmic bytes N * (12 + 8 C) summed over launches.
+  void set_gather_timing(bool on);
+  void gather_stats(double* ms, long long* launches, double* bytes);
 
  private:
   Problem prob_;
@@ -172,6 +179,9 @@ class Engine {
   DevBuf<double2> btmp_;      // band temporaries: 12 band vectors
   DevBuf<double2> src_;       // (nt+1) band vectors (incremental sources)
   DevBuf<double2> dseries_;   // (nt+1) band vectors (hessvec du / drho series)
+  DevBuf<double> f64a_, f64b_, f64c_, dker_;  // fp64 grid scratch (image constants), derivative kernels
+  DevBuf<float> maps_du_;     // 9 derivative fields for the Jacobian (allocated on first use)
+  DevBuf<double2> opt_ws_;    // optimizer workspace: 9 velocities
 
   void build_plan(DftPlan& p, const int* Ngrid, const int* K, const double* parent_wunit);
   void free_plans();
@@ -198,6 +208,12 @@ class Engine {
                      const double2* add, double beta);
 
   double reduce(int nparts, int op);
+  void timed_gather(const float* coef, int ncomp, const float* dep, float* out);
+
+  bool gt_on_ = false;
+  std::vector<cudaEvent_t> gt_events_;
+  std::vector<double> gt_bytes_;
+  size_t gt_used_ = 0;
   void count(int n = 1) { launches_ += n; }
 };
 

@@ -20,9 +20,14 @@ struct PcgInfo {
   std::vector<double> residuals;
 };
 
-struct Workspace {
-  DevBuf<double2> g, rhs, dv, x, r, z, p, hp, trial;
-  explicit Workspace(long long n) : g(n), rhs(n), dv(n), x(n), r(n), z(n), p(n), hp(n), trial(n) {}
+struct Vec {
+  double2* p;
+};
+struct Workspace {  // views of the engine's persistent optimizer workspace
+  Vec g, rhs, dv, x, r, z, p, hp, trial;
+  explicit Workspace(Engine& e)
+      : g{e.opt_ws(0)}, rhs{e.opt_ws(1)}, dv{e.opt_ws(2)}, x{e.opt_ws(3)}, r{e.opt_ws(4)}, z{e.opt_ws(5)},
+        p{e.opt_ws(6)}, hp{e.opt_ws(7)}, trial{e.opt_ws(8)} {}
 };
 
 // optimizer.hpp:86-120; x = 0, r = rhs, z = L^-1 r, p = z
@@ -76,7 +81,7 @@ double trial_energy(Engine& e, const double2* v, OptimizeResult& res) {
 OptimizeResult optimize(Engine& e, double2* v, const OptimizeOptions& opt) {
   OptimizeResult out;
   const long long n = e.vel_elems();
-  Workspace w(n);
+  Workspace w(e);
   const double mse_denom = e.mse_denominator();
   const double cellvol = e.problem().spacing[0] * e.problem().spacing[1] * e.problem().spacing[2];
   auto mse_rel = [&]() { return mse_denom > 0.0 ? e.residual_sumsq() * cellvol / mse_denom : 0.0; };

@@ -118,6 +118,11 @@ def lib():
             getattr(L, name).argtypes = args
             getattr(L, name).restype = C.c_int
         L.lddmm_default_options.argtypes = [C.POINTER(_Options)]
+        L.lddmm_stream.restype = C.c_void_p
+        L.lddmm_stream.argtypes = [vp]
+        L.lddmm_gather_timing.argtypes = [vp, C.c_int]
+        L.lddmm_gather_stats.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong),
+                                         C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -277,6 +282,20 @@ class Context:
     @property
     def vel_shape(self):
         return (self.nodes, 3) + tuple(self.band.bounds)
+
+    def stream_ptr(self):
+        return int(lib().lddmm_stream(self.h))
+
+    def sync(self):
+        self.check(lib().lddmm_sync(self.h))
+
+    def gather_timing(self, on=True):
+        self.check(lib().lddmm_gather_timing(self.h, int(on)))
+
+    def gather_stats(self):
+        ms, n, b = C.c_double(), C.c_longlong(), C.c_double()
+        self.check(lib().lddmm_gather_stats(self.h, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
 
 
 def _raise(rc, msg, step=-1):
