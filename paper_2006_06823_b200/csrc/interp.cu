@@ -97,8 +97,191 @@ __global__ __launch_bounds__(256) void gather_cubic_kernel(const float* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory tiled gather.  A CTA owns an 8 x 8 x 32 block of output nodes
+// and stages the periodic 12 x 12 x 36 source box (halo 2) of up to 3
+// components at a time.  With |floor(d)| <= 1 per axis (departure CFL < 1,
+// the regime SL runs in) every 64-tap stencil lies in the box: each tap is one
+// conflict-free LDS (a warp covers 32 consecutive z of one row) instead of an
+// L1 global load whose lanes straddle rows.  Points outside that regime read
+// their taps from global memory (same arithmetic, same order).
+constexpr int GT_X = 8, GT_Y = 8, GT_Z = 32, GT_H = 2;
+constexpr int GS_X = GT_X + 2 * GT_H, GS_Y = GT_Y + 2 * GT_H;
+// z pitch of a staged row is 64 words (36 used): rows differ by multiples of 32
+// banks, so a warp whose lanes straddle two rows (floor(d) changes along z) stays
+// bank-conflict free.
+constexpr int GS_ZUSED = GT_Z + 2 * GT_H, GS_Z = 64;
+constexpr int GS_VOL = GS_X * GS_Y * GS_Z;
+constexpr int GT_THREADS = 512;
+constexpr int GT_PTS = GT_X * GT_Y * GT_Z / GT_THREADS;  // 4 points per thread
+
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// one cubic weight (same expressions as cubic_w)
+__device__ __forceinline__ float cubic_w1(float t, int a) {
+  const float t2 = t * t, t3 = t2 * t;
+  if (a == 0) return (1.0f - 3.0f * t + 3.0f * t2 - t3) * (1.0f / 6.0f);
+  if (a == 1) return (4.0f - 6.0f * t2 + 3.0f * t3) * (1.0f / 6.0f);
+  if (a == 2) return (1.0f + 3.0f * t + 3.0f * t2 - 3.0f * t3) * (1.0f / 6.0f);
+  return t3 * (1.0f / 6.0f);
+}
+
+// Out-of-tile point (|floor(d)| > 1 on some axis): taps straight from global memory,
+// compact loops (rare path; keeps the register budget of the tiled kernel).
+template <int FG>
+__device__ __forceinline__ void gather_point_global(const float* __restrict__ coef, const float* __restrict__ disp,
+                                                    int i, int j, int k, int Nx, int Ny, int Nz, int nc, float* v) {
+  const long long N = (long long)Nx * Ny * Nz;
+  const long long p = ((long long)i * Ny + j) * Nz + k;
+  const float dx = __ldg(disp + p), dy = __ldg(disp + N + p), dz = __ldg(disp + 2 * N + p);
+  const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
+  const float tx = dx - fx, ty = dy - fy, tz = dz - fz;
+  const int xb = i + (int)fx - 1, yb = j + (int)fy - 1, zb = k + (int)fz - 1;
+  for (int c = 0; c < FG; ++c) v[c] = 0.f;
+#pragma unroll 1
+  for (int a = 0; a < 4; ++a) {
+    const float wa = cubic_w1(tx, a);
+    const int ix = wrapi(xb + a, Nx);
+#pragma unroll 1
+    for (int b = 0; b < 4; ++b) {
+      const float w01 = wa * cubic_w1(ty, b);
+      const long long row = ((long long)ix * Ny + wrapi(yb + b, Ny)) * Nz;
+      const int z0 = wrapi(zb, Nz), z1 = wrapi(zb + 1, Nz), z2 = wrapi(zb + 2, Nz), z3 = wrapi(zb + 3, Nz);
+      for (int c = 0; c < nc; ++c) {
+        const float* r = coef + c * N + row;
+        float pp = cubic_w1(tz, 0) * __ldg(r + z0);
+        pp = fmaf(cubic_w1(tz, 1), __ldg(r + z1), pp);
+        pp = fmaf(cubic_w1(tz, 2), __ldg(r + z2), pp);
+        pp = fmaf(cubic_w1(tz, 3), __ldg(r + z3), pp);
+        v[c] = fmaf(w01, pp, v[c]);
+      }
+    }
+  }
+}
+
+template <int FG>
+__global__ __launch_bounds__(GT_THREADS, 2) void gather_tiled_kernel(const float* __restrict__ coef, int F,
+                                                                  const float* __restrict__ disp,
+                                                                  float* __restrict__ out, int Nx, int Ny, int Nz) {
+  extern __shared__ float sm[];
+  const long long N = (long long)Nx * Ny * Nz;
+  const int x0 = blockIdx.x * GT_X, y0 = blockIdx.y * GT_Y, z0 = blockIdx.z * GT_Z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // this thread's points: rows warp*4 .. warp*4+3 of the 64 (x, y) rows, z = z0 + lane;
+  // the (cheap) per-point stencil set-up is redone per component group so that no
+  // per-point state is carried in registers across the staging barriers.
+  for (int c0 = 0; c0 < F; c0 += FG) {
+    const int nc = min(FG, F - c0);
+    __syncthreads();
+    {
+      // one warp per staged row: lanes copy z = z0-2 .. z0+33 (wrapped) with
+      // cp.async (LDGSTS), all rows in flight before one wait
+      const int gz0 = wrapi(z0 - GT_H + lane, Nz);
+      const int gz1 = wrapi(z0 - GT_H + 32 + (lane & 3), Nz);
+      for (int row = warp; row < nc * GS_X * GS_Y; row += GT_THREADS / 32) {
+        const int c = row / (GS_X * GS_Y);
+        const int rr = row - c * (GS_X * GS_Y);
+        const int ix = rr / GS_Y, jy = rr % GS_Y;
+        const float* src = coef + (c0 + c) * N +
+                           ((long long)wrapi(x0 - GT_H + ix, Nx) * Ny + wrapi(y0 - GT_H + jy, Ny)) * Nz;
+        float* dst = sm + c * GS_VOL + rr * GS_Z;
+        cp_async4(dst + lane, src + gz0);
+        if (lane < GS_ZUSED - 32) cp_async4(dst + 32 + lane, src + gz1);
+      }
+      cp_async_wait_all();
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int q = 0; q < GT_PTS; ++q) {
+      const int r = warp * GT_PTS + q;
+      const int rx = r / GT_Y, ry = r % GT_Y;
+      const int i = x0 + rx, j = y0 + ry, k = z0 + lane;
+      if (i >= Nx || j >= Ny || k >= Nz) continue;
+      const long long p = ((long long)i * Ny + j) * Nz + k;
+      const float dx = __ldg(disp + p), dy = __ldg(disp + N + p), dz = __ldg(disp + 2 * N + p);
+      const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
+      float v[FG];
+      if (fx >= -1.f && fx <= 0.f && fy >= -1.f && fy <= 0.f && fz >= -1.f && fz <= 0.f) {
+        // x, y: the 4 rows selected by floor(d); z: a fixed 5-tap window z-2..z+2
+        // (one weight exactly zero), so a warp's 32 lanes always read 32
+        // consecutive words -> conflict-free whatever floor(dz) does along z.  The
+        // zero-weight tap comes first or last, so the sum is bitwise the 4-tap one.
+        const int lb = ((rx + GT_H + (int)fx - 1) * GS_Y + (ry + GT_H + (int)fy - 1)) * GS_Z + lane;
+        float wx[4], wy[4], w4[4], wz[5];
+        cubic_w(dx - fx, wx);
+        cubic_w(dy - fy, wy);
+        cubic_w(dz - fz, w4);
+        const bool lo = fz < 0.f;  // taps z-2..z+1
+        wz[0] = lo ? w4[0] : 0.f;
+        wz[1] = lo ? w4[1] : w4[0];
+        wz[2] = lo ? w4[2] : w4[1];
+        wz[3] = lo ? w4[3] : w4[2];
+        wz[4] = lo ? 0.f : w4[3];
+#pragma unroll
+        for (int c = 0; c < FG; ++c) v[c] = 0.f;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int row = lb + (a * GS_Y + b) * GS_Z;
+            const float w01 = wx[a] * wy[b];
+#pragma unroll
+            for (int c = 0; c < FG; ++c) {
+              const float* rr = sm + c * GS_VOL + row;
+              float pp = wz[0] * rr[0];
+              pp = fmaf(wz[1], rr[1], pp);
+              pp = fmaf(wz[2], rr[2], pp);
+              pp = fmaf(wz[3], rr[3], pp);
+              pp = fmaf(wz[4], rr[4], pp);
+              v[c] = fmaf(w01, pp, v[c]);
+            }
+          }
+        }
+      } else {
+        gather_point_global<FG>(coef + c0 * N, disp, i, j, k, Nx, Ny, Nz, nc, v);
+      }
+#pragma unroll
+      for (int c = 0; c < FG; ++c)
+        if (c < nc) out[(c0 + c) * N + p] = v[c];
+    }
+  }
+}
+
 void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float* out, const int* N,
                          cudaStream_t s) {
+  {
+    const int FG = ncomp >= 3 ? 3 : ncomp;
+    dim3 grid(ceil_div(N[0], GT_X), ceil_div(N[1], GT_Y), ceil_div(N[2], GT_Z));
+    const size_t smem = (size_t)FG * GS_VOL * sizeof(float);
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    LDDMM_CUDA(cudaGetDevice(&dev));
+    if (!attr_set[dev & 63]) {
+      LDDMM_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      3 * GS_VOL * (int)sizeof(float)));
+      LDDMM_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      2 * GS_VOL * (int)sizeof(float)));
+      LDDMM_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      1 * GS_VOL * (int)sizeof(float)));
+      attr_set[dev & 63] = true;
+    }
+    if (FG == 3)
+      gather_tiled_kernel<3><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2]);
+    else if (FG == 2)
+      gather_tiled_kernel<2><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2]);
+    else
+      gather_tiled_kernel<1><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2]);
+    LDDMM_LAUNCH_CHECK();
+    return;
+  }
+}
+
+void launch_gather_cubic_global(const float* coef, int ncomp, const float* disp, float* out, const int* N,
+                                cudaStream_t s) {
   const long long n = (long long)N[0] * N[1] * N[2];
   const int grid = grid_for(n, 256, 16);
   int done = 0;
