@@ -182,6 +182,11 @@ int lddmm_op_departure(lddmm_ctx* ctx, const double* dev_v, float* dev_dep_fwd, 
 /* truncated products (spectral.hpp:460-510): op 0 star(s,s) 1 star(s,vec)
  * 2 star_dot 3 band_jac_mul 4 band_jacT_mul ; 5 band_divergence(vec) */
 int lddmm_op_band(lddmm_ctx* ctx, int op, const double* dev_a, const double* dev_b, double* dev_out);
+/* the SL cubic gather alone (ScalarSampler::eval_cubic at departure points, interp.hpp:119-159):
+ * dev_coef [ncomp][N] spline coefficients, dev_dep [3][N] grid-unit displacements;
+ * impl 0 production (register-window), 1 smem-tiled, 2 global-memory (all bitwise equal) */
+int lddmm_op_gather(lddmm_ctx* ctx, int impl, const float* dev_coef, int ncomp, const float* dev_dep,
+                    float* dev_out);
 /* cubic pull-back of grid scalar fields through x - disp (warp with
  * points_from_displacement, interp.hpp:178-210, variants.hpp:49-51); disp phys units */
 int lddmm_op_warp(lddmm_ctx* ctx, const float* dev_field, int ncomp, const float* dev_disp, float* dev_out);

@@ -368,6 +368,20 @@ int lddmm_op_band(lddmm_ctx* ctx, int op, const double* a, const double* b, doub
   });
 }
 
+int lddmm_op_gather(lddmm_ctx* ctx, int impl, const float* coef, int ncomp, const float* dep, float* out) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    int N[3] = {e.problem().dims[0], e.problem().dims[1], e.problem().dims[2]};
+    if (impl == 0)
+      launch_gather_cubic(coef, ncomp, dep, out, N, e.stream());
+    else if (impl == 1)
+      launch_gather_cubic_tiled(coef, ncomp, dep, out, N, e.stream());
+    else
+      launch_gather_cubic_global(coef, ncomp, dep, out, N, e.stream());
+    e.sync();
+  });
+}
+
 int lddmm_op_warp(lddmm_ctx* ctx, const float* field, int ncomp, const float* disp, float* out) {
   return guard(ctx, [&] {
     ctx->eng->warp_grid(field, ncomp, disp, out);

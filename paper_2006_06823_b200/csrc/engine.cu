@@ -456,8 +456,8 @@ void Engine::provider_build(const double2* v, ProviderState& ps, bool with_bwd) 
   const int g = launch_absmax_partial(3 * N, gridA_.p, part_.p, stream_);
   launch_reduce_final(part_, g, 1, slots_.p + 1, stream_);
   const double dt = 1.0 / prob_.nt;
-  launch_departure(gridA_.p, gridA_.p + 3 * N, dt, h_, ps.dep_fwd.p, with_bwd ? ps.dep_bwd.p : nullptr, full_.N,
-                   stream_);
+  launch_departure(gridA_.p, gridA_.p + 3 * N, dt, h_, ps.dep_fwd.p, with_bwd ? ps.dep_bwd.p : nullptr, gridB_.p,
+                   full_.N, stream_);
   ps.has_bwd = with_bwd;
   LDDMM_CUDA(cudaMemcpyAsync(host_slots_ + 1, slots_.p + 1, sizeof(double), cudaMemcpyDeviceToHost, stream_));
   sync();

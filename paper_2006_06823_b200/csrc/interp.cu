@@ -6,6 +6,8 @@
 // points are carried as DISPLACEMENTS in grid units (X = x + d*h) instead of
 // the reference's absolute physical coordinates: floor(i + d) = i + floor(d)
 // exactly, so the fp32 weights lose nothing to large coordinates.
+#include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -119,6 +121,10 @@ __device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(float* smem, const float* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // one cubic weight (same expressions as cubic_w)
@@ -134,10 +140,11 @@ __device__ __forceinline__ float cubic_w1(float t, int a) {
 // compact loops (rare path; keeps the register budget of the tiled kernel).
 template <int FG>
 __device__ __forceinline__ void gather_point_global(const float* __restrict__ coef, const float* __restrict__ disp,
-                                                    int i, int j, int k, int Nx, int Ny, int Nz, int nc, float* v) {
+                                                    int i, int j, int k, int Nx, int Ny, int Nz, int nc, float* v,
+                                                    float3 sc) {
   const long long N = (long long)Nx * Ny * Nz;
   const long long p = ((long long)i * Ny + j) * Nz + k;
-  const float dx = __ldg(disp + p), dy = __ldg(disp + N + p), dz = __ldg(disp + 2 * N + p);
+  const float dx = sc.x * __ldg(disp + p), dy = sc.y * __ldg(disp + N + p), dz = sc.z * __ldg(disp + 2 * N + p);
   const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
   const float tx = dx - fx, ty = dy - fy, tz = dz - fz;
   const int xb = i + (int)fx - 1, yb = j + (int)fy - 1, zb = k + (int)fz - 1;
@@ -166,7 +173,8 @@ __device__ __forceinline__ void gather_point_global(const float* __restrict__ co
 template <int FG>
 __global__ __launch_bounds__(GT_THREADS, 2) void gather_tiled_kernel(const float* __restrict__ coef, int F,
                                                                   const float* __restrict__ disp,
-                                                                  float* __restrict__ out, int Nx, int Ny, int Nz) {
+                                                                  float* __restrict__ out, int Nx, int Ny, int Nz,
+                                                                  float3 sc) {
   extern __shared__ float sm[];
   const long long N = (long long)Nx * Ny * Nz;
   const int x0 = blockIdx.x * GT_X, y0 = blockIdx.y * GT_Y, z0 = blockIdx.z * GT_Z;
@@ -202,7 +210,7 @@ __global__ __launch_bounds__(GT_THREADS, 2) void gather_tiled_kernel(const float
       const int i = x0 + rx, j = y0 + ry, k = z0 + lane;
       if (i >= Nx || j >= Ny || k >= Nz) continue;
       const long long p = ((long long)i * Ny + j) * Nz + k;
-      const float dx = __ldg(disp + p), dy = __ldg(disp + N + p), dz = __ldg(disp + 2 * N + p);
+      const float dx = sc.x * __ldg(disp + p), dy = sc.y * __ldg(disp + N + p), dz = sc.z * __ldg(disp + 2 * N + p);
       const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
       float v[FG];
       if (fx >= -1.f && fx <= 0.f && fy >= -1.f && fy <= 0.f && fz >= -1.f && fz <= 0.f) {
@@ -242,7 +250,7 @@ __global__ __launch_bounds__(GT_THREADS, 2) void gather_tiled_kernel(const float
           }
         }
       } else {
-        gather_point_global<FG>(coef + c0 * N, disp, i, j, k, Nx, Ny, Nz, nc, v);
+        gather_point_global<FG>(coef + c0 * N, disp, i, j, k, Nx, Ny, Nz, nc, v, sc);
       }
 #pragma unroll
       for (int c = 0; c < FG; ++c)
@@ -251,8 +259,289 @@ __global__ __launch_bounds__(GT_THREADS, 2) void gather_tiled_kernel(const float
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-window gather (the production path).  A CTA owns TX x TY full
+// z-rows of output nodes and stages the periodic (TX+4) x (TY+4) source rows of
+// FG components per stage in shared memory (row pitch RL >= Nz + 4, z halo 2),
+// double-buffered across component groups (cp.async commit groups) so the
+// staging of group g+1 overlaps the arithmetic of group g.  A thread evaluates
+// FOUR consecutive z nodes of one row: for every source row of the 5 x 5 (x, y)
+// neighbourhood it loads one aligned 8-float window (two LDS.128) covering the
+// 5-tap z stencils of the four nodes, so the shared-memory traffic per node and
+// component is 25 x 2 floats instead of 64-80.  Every axis uses the fixed
+// 5-tap window [-2, 2] with the zero weight first or last (|floor(d)| <= 1, the
+// SL regime): the sum is bitwise the reference's 4-tap accumulate<4>
+// (interp.hpp:145-156), same x-outer / y-inner order.  Nodes outside that
+// regime fall back to the global-memory path.
+constexpr int GW_H = 2;
+
+__device__ __forceinline__ void w5(float d, float f, float* w) {
+  float w4[4];
+  cubic_w(d - f, w4);
+  const bool lo = f < 0.f;  // taps -2..1, else -1..2
+  w[0] = lo ? w4[0] : 0.f;
+  w[1] = lo ? w4[1] : w4[0];
+  w[2] = lo ? w4[2] : w4[1];
+  w[3] = lo ? w4[3] : w4[2];
+  w[4] = lo ? 0.f : w4[3];
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
+}
+
+template <int TX, int TY, int NTH>
+__device__ __forceinline__ void gw_stage(float* dst_base, const float* __restrict__ coef, long long N, int c0, int nc,
+                                         int x0, int y0, int Nx, int Ny, int Nz, int RL) {
+  constexpr int SX = TX + 2 * GW_H, SY = TY + 2 * GW_H;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cvol = SX * SY * RL;
+  for (int row = warp; row < nc * SX * SY; row += NTH / 32) {
+    const int c = row / (SX * SY);
+    const int rr = row - c * (SX * SY);
+    const int ix = rr / SY, jy = rr - (rr / SY) * SY;
+    const float* src =
+        coef + (c0 + c) * N + ((long long)wrapi(x0 - GW_H + ix, Nx) * Ny + wrapi(y0 - GW_H + jy, Ny)) * Nz;
+    float* dst = dst_base + c * cvol + rr * RL;
+    // 8-byte copies: Nz is even, so every pair (z, z+1), z = zz - 2 even, is contiguous
+    // in global memory even across the periodic wrap
+    for (int zz = 2 * lane; zz < RL; zz += 64) {
+      int gz = zz - GW_H;
+      gz += gz < 0 ? Nz : 0;
+      gz -= gz >= Nz ? Nz : 0;
+      cp_async8(dst + zz, src + gz);
+    }
+  }
+}
+
+template <int FG, int TX, int TY, int NTH>
+__device__ __forceinline__ void gw_compute(const float* sbuf, const float* __restrict__ coef,
+                                           const float* __restrict__ disp, float* __restrict__ out, long long N,
+                                           int c0, int nc, int x0, int y0, int Nx, int Ny, int Nz, int RL,
+                                           float3 sc) {
+  constexpr int SY = TY + 2 * GW_H, SX = TX + 2 * GW_H;
+  const int cvol = SX * SY * RL;
+  const int G = (Nz + 3) >> 2;
+  const int items = TX * TY * G;
+  const bool vec = (Nz & 3) == 0;
+  for (int it = threadIdx.x; it < items; it += NTH) {
+    const int r = it / G, g = it - r * G;
+    const int rx = r / TY, ry = r - (r / TY) * TY;
+    const int i = x0 + rx, j = y0 + ry;
+    if (i >= Nx || j >= Ny) continue;
+    const int z = g << 2;
+    const int npt = min(4, Nz - z);
+    const long long p0 = ((long long)i * Ny + j) * Nz + z;
+    float dx[4], dy[4], dz[4];
+    if (vec) {
+      const float4 a = *reinterpret_cast<const float4*>(disp + p0);
+      const float4 b = *reinterpret_cast<const float4*>(disp + N + p0);
+      const float4 cc = *reinterpret_cast<const float4*>(disp + 2 * N + p0);
+      dx[0] = a.x; dx[1] = a.y; dx[2] = a.z; dx[3] = a.w;
+      dy[0] = b.x; dy[1] = b.y; dy[2] = b.z; dy[3] = b.w;
+      dz[0] = cc.x; dz[1] = cc.y; dz[2] = cc.z; dz[3] = cc.w;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        dx[m] *= sc.x;
+        dy[m] *= sc.y;
+        dz[m] *= sc.z;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const bool in = m < npt;
+        dx[m] = in ? sc.x * __ldg(disp + p0 + m) : 0.f;
+        dy[m] = in ? sc.y * __ldg(disp + N + p0 + m) : 0.f;
+        dz[m] = in ? sc.z * __ldg(disp + 2 * N + p0 + m) : 0.f;
+      }
+    }
+    float fx[4], fy[4], fz[4];
+    bool ok = true;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      fx[m] = floorf(dx[m]);
+      fy[m] = floorf(dy[m]);
+      fz[m] = floorf(dz[m]);
+      ok = ok && fx[m] >= -1.f && fx[m] <= 0.f && fy[m] >= -1.f && fy[m] <= 0.f && fz[m] >= -1.f && fz[m] <= 0.f;
+    }
+    if (!ok) {
+      for (int m = 0; m < npt; ++m) {
+        float v[FG];
+        gather_point_global<FG>(coef + c0 * N, disp, i, j, z + m, Nx, Ny, Nz, nc, v, sc);
+        for (int c = 0; c < nc; ++c) out[(c0 + c) * N + p0 + m] = v[c];
+      }
+      continue;
+    }
+    // weights of node pairs (0,1) and (2,3) packed as float2 for the sm_100 packed
+    // FFMA2 pipe: each __ffma2_rn is two independent, correctly rounded fmaf.
+    float2 wx[2][5], wy[2][5], wz[2][5];
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) {
+      float t0[5], t1[5];
+      w5(dx[2 * hp], fx[2 * hp], t0);
+      w5(dx[2 * hp + 1], fx[2 * hp + 1], t1);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) wx[hp][k] = make_float2(t0[k], t1[k]);
+      w5(dy[2 * hp], fy[2 * hp], t0);
+      w5(dy[2 * hp + 1], fy[2 * hp + 1], t1);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) wy[hp][k] = make_float2(t0[k], t1[k]);
+      w5(dz[2 * hp], fz[2 * hp], t0);
+      w5(dz[2 * hp + 1], fz[2 * hp + 1], t1);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) wz[hp][k] = make_float2(t0[k], t1[k]);
+    }
+    float2 acc[FG][2];
+#pragma unroll
+    for (int c = 0; c < FG; ++c) acc[c][0] = acc[c][1] = make_float2(0.f, 0.f);
+    const float* base = sbuf + (rx * SY + ry) * RL + z;
+#pragma unroll
+    for (int a = 0; a < 5; ++a) {
+#pragma unroll
+      for (int b = 0; b < 5; ++b) {
+        const float* rowp = base + (a * SY + b) * RL;
+        const float2 w01a = __fmul2_rn(wx[0][a], wy[0][b]);
+        const float2 w01b = __fmul2_rn(wx[1][a], wy[1][b]);
+#pragma unroll
+        for (int c = 0; c < FG; ++c) {
+          if (c < nc) {
+            const float4 A = *reinterpret_cast<const float4*>(rowp + c * cvol);
+            const float4 B = *reinterpret_cast<const float4*>(rowp + c * cvol + 4);
+            const float win[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+            // nodes (0,1): taps win[k], win[k+1]; nodes (2,3): win[k+2], win[k+3]
+            float2 pa = __fmul2_rn(wz[0][0], make_float2(win[0], win[1]));
+            float2 pb = __fmul2_rn(wz[1][0], make_float2(win[2], win[3]));
+#pragma unroll
+            for (int k = 1; k < 5; ++k) {
+              pa = __ffma2_rn(wz[0][k], make_float2(win[k], win[k + 1]), pa);
+              pb = __ffma2_rn(wz[1][k], make_float2(win[k + 2], win[k + 3]), pb);
+            }
+            acc[c][0] = __ffma2_rn(w01a, pa, acc[c][0]);
+            acc[c][1] = __ffma2_rn(w01b, pb, acc[c][1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < FG; ++c) {
+      if (c >= nc) break;
+      float* o = out + (c0 + c) * N + p0;
+      if (vec) {
+        *reinterpret_cast<float4*>(o) = make_float4(acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y);
+      } else {
+        const float v4[4] = {acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y};
+        for (int m = 0; m < npt; ++m) o[m] = v4[m];
+      }
+    }
+  }
+}
+
+// NBUF = 1: stage FG components, compute, repeat.  NBUF = 2: double-buffered.
+template <int FG, int TX, int TY, int NTH, int MINB, int NBUF>
+__global__ __launch_bounds__(NTH, MINB) void gather_win_kernel(const float* __restrict__ coef, int F,
+                                                               const float* __restrict__ disp,
+                                                               float* __restrict__ out, int Nx, int Ny, int Nz,
+                                                               int RL, float3 sc) {
+  extern __shared__ __align__(16) float smw[];
+  constexpr int SX = TX + 2 * GW_H, SY = TY + 2 * GW_H;
+  const long long N = (long long)Nx * Ny * Nz;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int bufvol = FG * SX * SY * RL;
+  const int ngroups = (F + FG - 1) / FG;
+  if (NBUF == 1) {
+    for (int gi = 0; gi < ngroups; ++gi) {
+      const int c0 = gi * FG, nc = min(FG, F - c0);
+      __syncthreads();
+      gw_stage<TX, TY, NTH>(smw, coef, N, c0, nc, x0, y0, Nx, Ny, Nz, RL);
+      cp_async_commit();
+      cp_async_wait_group<0>();
+      __syncthreads();
+      gw_compute<FG, TX, TY, NTH>(smw, coef, disp, out, N, c0, nc, x0, y0, Nx, Ny, Nz, RL, sc);
+    }
+  } else {
+    gw_stage<TX, TY, NTH>(smw, coef, N, 0, min(FG, F), x0, y0, Nx, Ny, Nz, RL);
+    cp_async_commit();
+    for (int gi = 0; gi < ngroups; ++gi) {
+      const int c0 = gi * FG, nc = min(FG, F - c0);
+      if (gi + 1 < ngroups) {
+        const int c1 = c0 + FG;
+        gw_stage<TX, TY, NTH>(smw + ((gi + 1) & 1) * bufvol, coef, N, c1, min(FG, F - c1), x0, y0, Nx, Ny, Nz,
+                              RL);
+        cp_async_commit();
+        cp_async_wait_group<1>();
+      } else {
+        cp_async_wait_group<0>();
+      }
+      __syncthreads();
+      gw_compute<FG, TX, TY, NTH>(smw + (gi & 1) * bufvol, coef, disp, out, N, c0, nc, x0, y0, Nx, Ny, Nz, RL,
+                                  sc);
+      __syncthreads();
+    }
+  }
+}
+
+static int gw_row_len(int Nz) { return (((Nz + 3) >> 2) << 2) + 4; }
+
+template <int FG, int TX, int TY, int NTH, int MINB, int NBUF>
+static void launch_gw(const float* coef, int ncomp, const float* disp, float* out, const int* N, int RL,
+                      float3 sc, cudaStream_t s) {
+  auto kern = gather_win_kernel<FG, TX, TY, NTH, MINB, NBUF>;
+  const size_t smem = (size_t)NBUF * FG * (TX + 4) * (TY + 4) * RL * sizeof(float);
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  LDDMM_CUDA(cudaGetDevice(&dev));
+  if (!attr_set[dev & 63]) {
+    LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set[dev & 63] = true;
+  }
+  dim3 grid(ceil_div(N[0], TX), ceil_div(N[1], TY), 1);
+  kern<<<grid, NTH, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], RL, sc);
+  LDDMM_LAUNCH_CHECK();
+}
+
+// Gather variant (env LDDMM_GATHER, default 1): 1 = single-buffered FG=3 8x4 tiles
+// (1 CTA/SM); 2 = double-buffered FG=1 4x4 tiles (2 CTAs/SM).
+static int gather_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LDDMM_GATHER");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float* out, const int* N,
                          cudaStream_t s) {
+  launch_gather_scaled(coef, ncomp, disp, 1.f, 1.f, 1.f, out, N, s);
+}
+
+void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
+                          const int* N, cudaStream_t s) {
+  const float3 sc = make_float3(sx, sy, sz);
+  const int RL = gw_row_len(N[2]);
+  const size_t smem_max = 227 * 1024;
+  const int var = gather_variant();
+  if (var == 2 && 2 * 8 * 8 * (size_t)RL * 4 <= smem_max / 2) {
+    launch_gw<1, 4, 4, 256, 2, 2>(coef, ncomp, disp, out, N, RL, sc, s);
+    return;
+  }
+  const size_t per_comp = (size_t)12 * 8 * RL * sizeof(float);
+  int FG = (int)std::min<size_t>(3, smem_max / per_comp);
+  if (FG > ncomp) FG = ncomp;
+  if (FG == 3)
+    launch_gw<3, 8, 4, 512, 1, 1>(coef, ncomp, disp, out, N, RL, sc, s);
+  else if (FG == 2)
+    launch_gw<2, 8, 4, 512, 1, 1>(coef, ncomp, disp, out, N, RL, sc, s);
+  else if (FG == 1)
+    launch_gw<1, 8, 4, 512, 1, 1>(coef, ncomp, disp, out, N, RL, sc, s);
+  else
+    launch_gather_cubic_tiled(coef, ncomp, disp, out, N, s);  // (unit scale only: huge grids)
+}
+
+void launch_gather_cubic_tiled(const float* coef, int ncomp, const float* disp, float* out, const int* N,
+                               cudaStream_t s) {
   {
     const int FG = ncomp >= 3 ? 3 : ncomp;
     dim3 grid(ceil_div(N[0], GT_X), ceil_div(N[1], GT_Y), ceil_div(N[2], GT_Z));
@@ -270,11 +559,11 @@ void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float*
       attr_set[dev & 63] = true;
     }
     if (FG == 3)
-      gather_tiled_kernel<3><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2]);
+      gather_tiled_kernel<3><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
     else if (FG == 2)
-      gather_tiled_kernel<2><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2]);
+      gather_tiled_kernel<2><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
     else
-      gather_tiled_kernel<1><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2]);
+      gather_tiled_kernel<1><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
     LDDMM_LAUNCH_CHECK();
     return;
   }
@@ -334,53 +623,40 @@ __global__ __launch_bounds__(256) void departure_kernel(const float* __restrict_
   }
 }
 
-void launch_departure(const float* vgrid, const float* vcoef, double dt, const double* h, float* dep_fwd,
-                      float* dep_bwd, const int* N, cudaStream_t s) {
-  const long long n = (long long)N[0] * N[1] * N[2];
-  departure_kernel<<<grid_for(n, 256, 16), 256, 0, s>>>(vgrid, vcoef, (float)(dt / h[0]), (float)(dt / h[1]),
-                                                        (float)(dt / h[2]), dep_fwd, dep_bwd, N[0], N[1], N[2]);
-  LDDMM_LAUNCH_CHECK();
-}
-
-// ---------------------------------------------------------------------------
-// pull-back through points x - disp (disp physical), used for m1 = I0 o phi1 etc.
-
-template <int F>
-__global__ __launch_bounds__(256) void warp_disp_kernel(const float* __restrict__ coef,
-                                                        const float* __restrict__ disp, float ihx, float ihy,
-                                                        float ihz, float* __restrict__ out, int Nx, int Ny,
-                                                        int Nz) {
-  const long long N = (long long)Nx * Ny * Nz;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(p % Nz);
-    const long long q = p / Nz;
-    const int j = (int)(q % Ny);
-    const int i = (int)(q / Ny);
-    Stencil s;
-    make_stencil(i, j, k, -__ldg(disp + p) * ihx, -__ldg(disp + N + p) * ihy, -__ldg(disp + 2 * N + p) * ihz, Nx,
-                 Ny, Nz, s);
-    float v[F];
-    sample<F>(coef, N, Ny, Nz, s, v);
-#pragma unroll
-    for (int c = 0; c < F; ++c) out[c * N + p] = v[c];
+// D = sg * dt/2 * (v_traced(X*) + v_grid) in grid units, vm = v_traced(X*) gathered
+__global__ void departure_combine_kernel(long long n, const float* __restrict__ vg, const float* __restrict__ vm,
+                                         float dtx, float dty, float dtz, float sg, float* __restrict__ o) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const float ux = vg[p] * dtx, uy = vg[n + p] * dty, uz = vg[2 * n + p] * dtz;
+    o[p] = sg * 0.5f * (vm[p] * dtx + ux);
+    o[n + p] = sg * 0.5f * (vm[n + p] * dty + uy);
+    o[2 * n + p] = sg * 0.5f * (vm[2 * n + p] * dtz + uz);
   }
 }
 
+// sl_departure (transport.hpp:83-102) for a stationary velocity: X* = x + sg dt v(x),
+// v_traced(X*) through the production gather (displacement scale sg dt / h), then the
+// trapezoid combination; scratch holds [3][N] floats per direction.
+void launch_departure(const float* vgrid, const float* vcoef, double dt, const double* h, float* dep_fwd,
+                      float* dep_bwd, float* scratch, const int* N, cudaStream_t s) {
+  const long long n = (long long)N[0] * N[1] * N[2];
+  const float dtx = (float)(dt / h[0]), dty = (float)(dt / h[1]), dtz = (float)(dt / h[2]);
+  for (int dir = 0; dir < (dep_bwd ? 2 : 1); ++dir) {
+    const float sg = dir == 0 ? -1.f : 1.f;
+    float* vm = scratch + dir * 3 * n;
+    launch_gather_scaled(vcoef, 3, vgrid, sg * dtx, sg * dty, sg * dtz, vm, N, s);
+    departure_combine_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, vgrid, vm, dtx, dty, dtz, sg,
+                                                              dir == 0 ? dep_fwd : dep_bwd);
+    LDDMM_LAUNCH_CHECK();
+  }
+}
+
+// pull-back through points x - disp (disp physical): the production gather with
+// displacement scale -1/h (m1 = I0 o phi1, grad_src_warped, warp of grid fields)
 void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp_phys, const double* h,
                                  float* out, const int* N, cudaStream_t s) {
-  const long long n = (long long)N[0] * N[1] * N[2];
-  const int grid = grid_for(n, 256, 16);
-  const float ix = (float)(1.0 / h[0]), iy = (float)(1.0 / h[1]), iz = (float)(1.0 / h[2]);
-  if (ncomp == 1)
-    warp_disp_kernel<1><<<grid, 256, 0, s>>>(coef, disp_phys, ix, iy, iz, out, N[0], N[1], N[2]);
-  else if (ncomp == 3)
-    warp_disp_kernel<3><<<grid, 256, 0, s>>>(coef, disp_phys, ix, iy, iz, out, N[0], N[1], N[2]);
-  else if (ncomp == 4)
-    warp_disp_kernel<4><<<grid, 256, 0, s>>>(coef, disp_phys, ix, iy, iz, out, N[0], N[1], N[2]);
-  else
-    throw EngineError(3, "warp_by_displacement: unsupported component count");
-  LDDMM_LAUNCH_CHECK();
+  launch_gather_scaled(coef, ncomp, disp_phys, -(float)(1.0 / h[0]), -(float)(1.0 / h[1]), -(float)(1.0 / h[2]),
+                       out, N, s);
 }
 
 // ---------------------------------------------------------------------------

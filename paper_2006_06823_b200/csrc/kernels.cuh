@@ -71,9 +71,17 @@ void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int l
 // out[c][i] = cubic B-spline sample of coef[c] at node i + disp[:, i] (grid units), c < ncomp
 void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float* out, const int* N,
                          cudaStream_t s);
+// alternative implementations of the same gather (tests / ablations)
+void launch_gather_cubic_tiled(const float* coef, int ncomp, const float* disp, float* out, const int* N,
+                               cudaStream_t s);
+void launch_gather_cubic_global(const float* coef, int ncomp, const float* disp, float* out, const int* N,
+                                cudaStream_t s);
 // grid-unit departure displacements for both directions (transport.hpp:83-102)
 void launch_departure(const float* vgrid, const float* vcoef, double dt, const double* h, float* dep_fwd,
-                      float* dep_bwd, const int* N, cudaStream_t s);
+                      float* dep_bwd, float* scratch, const int* N, cudaStream_t s);
+// gather with the displacement scaled per axis: samples coef at node + (sx dx, sy dy, sz dz)
+void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
+                          const int* N, cudaStream_t s);
 // cubic pull-back of coef at x - disp_phys where disp is a grid field in physical units
 // (points_from_displacement, variants.hpp:49-51); out[c] for ncomp coefficient fields
 void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp_phys, const double* h,

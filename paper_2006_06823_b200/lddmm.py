@@ -114,6 +114,7 @@ def lib():
             "lddmm_op_departure": [vp, vp, vp, vp, C.POINTER(C.c_double)],
             "lddmm_op_band": [vp, C.c_int, vp, vp, vp],
             "lddmm_op_warp": [vp, vp, C.c_int, vp, vp],
+            "lddmm_op_gather": [vp, C.c_int, vp, C.c_int, vp, vp],
         }.items():
             getattr(L, name).argtypes = args
             getattr(L, name).restype = C.c_int
@@ -556,6 +557,15 @@ class Ops:
         out = self.band_out(ncomp_out)
         self.ctx.check(lib().lddmm_op_band(self.ctx.h, int(op), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
                                            C.c_void_p(out.data_ptr())))
+        return out
+
+    def gather(self, coef, dep, impl=0):
+        coef = coef.to(self.torch.float32).contiguous()
+        dep = dep.to(self.torch.float32).contiguous()
+        nc = coef.shape[0]
+        out = self.grid_out(nc)
+        self.ctx.check(lib().lddmm_op_gather(self.ctx.h, int(impl), C.c_void_p(coef.data_ptr()), nc,
+                                             C.c_void_p(dep.data_ptr()), C.c_void_p(out.data_ptr())))
         return out
 
     def warp(self, f, disp):
