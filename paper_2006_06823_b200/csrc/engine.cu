@@ -188,6 +188,19 @@ void Engine::build_plan(DftPlan& p, const int* Ng, const int* K, const double* w
   p.wy_p = (float2*)upload(wy_p.data(), wy_p.size() * sizeof(float2));
   p.tz_e = (float*)upload(tz_e.data(), tz_e.size() * sizeof(float));
   p.tz_p = (float*)upload(tz_p.data(), tz_p.size() * sizeof(float));
+  auto alloc = [&](size_t n) {
+    void* d = nullptr;
+    LDDMM_CUDA(cudaMalloc(&d, n * sizeof(float)));
+    plan_allocs_.push_back(d);
+    return (float*)d;
+  };
+  p.tz_e_big = alloc(tz_e.size());
+  p.tz_e_small = alloc(tz_e.size());
+  p.tz_p_big = alloc(tz_p.size());
+  p.tz_p_small = alloc(tz_p.size());
+  launch_tf32_split(p.tz_e, p.tz_e_big, p.tz_e_small, (long long)tz_e.size(), stream_);
+  launch_tf32_split(p.tz_p, p.tz_p_big, p.tz_p_small, (long long)tz_p.size(), stream_);
+  sync();
 }
 
 void Engine::timed_gather(const float* coef, int ncomp, const float* dep, float* out) {

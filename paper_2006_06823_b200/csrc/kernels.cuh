@@ -52,6 +52,8 @@ struct DftPlan {
   float* tz_p = nullptr;   // [Nz][2H]  (cos, -sin)(2 pi kz z / Nz)
   float2* wx_p = nullptr;  // [Kx][Nx]  exp(-2 pi i kx x / Nx)
   float2* wy_p = nullptr;  // [Ky][Ny]
+  // TF32 big/small splits of the z tables for the tensor-core (3xTF32) z stages
+  float *tz_e_big = nullptr, *tz_e_small = nullptr, *tz_p_big = nullptr, *tz_p_small = nullptr;
   long long npts() const { return (long long)N[0] * N[1] * N[2]; }
   long long half() const { return (long long)K[0] * K[1] * (K[2] / 2); }
   long long kprod() const { return (long long)K[0] * K[1] * K[2]; }
@@ -65,6 +67,10 @@ void launch_sgemm(const float* A, int lda, long long sA, const float* B, int ldb
                   long long sC, int M, int N, int K, int batch, cudaStream_t s);
 void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int ldb, float2* C, long long sC,
                   int ldc, int M, int N, int K, int batch, cudaStream_t s);
+// 3xTF32 tensor-core GEMM C[b] = A[b] * B with B given as TF32 big/small parts (tc_gemm.cu)
+void launch_tc3_gemm(const float* A, int lda, long long sA, const float* Bbig, const float* Bsmall, int ldb, float* C,
+                     int ldc, long long sC, int M, int N, int K, int batch, cudaStream_t s);
+void launch_tf32_split(const float* in, float* big, float* small, long long n, cudaStream_t s);
 
 // ---- interpolation / transport -------------------------------------------------
 

@@ -20,6 +20,8 @@
 // X/Y stages are batched complex GEMMs against fp32 twiddle tables generated in
 // fp64; the Z stages are real GEMMs (K = Kz for embed, K = Nz for project).
 // All products accumulate in fp32.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -279,6 +281,16 @@ void launch_sgemm(const float* A, int lda, long long sA, const float* B, int ldb
   LDDMM_LAUNCH_CHECK();
 }
 
+// z stages on the tensor cores (3xTF32) unless LDDMM_TC=0
+static bool use_tensor_cores() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LDDMM_TC");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // embed nf half-band fields D[nf][Kx][Ky][H] -> grid fields out[nf][N] (fp32)
 void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2, float* out, cudaStream_t s) {
   const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
@@ -289,16 +301,24 @@ void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2
   launch_cgemm(p.wx_e, Kx, E1, (long long)Kx * Ny * H, Ny * H, E2, (long long)Nx * Ny * H, Ny * H, Nx, Ny * H,
                Kx, nf, s);
   // Z: for each f: out[(Nx Ny) x Nz] = E2 as float[(Nx Ny) x 2H] * Tz_e[2H x Nz]
-  launch_sgemm(reinterpret_cast<const float*>(E2), 2 * H, (long long)Nx * Ny * 2 * H, p.tz_e, Nz, out, Nz,
-               (long long)Nx * Ny * Nz, Nx * Ny, Nz, 2 * H, nf, s);
+  if (use_tensor_cores())
+    launch_tc3_gemm(reinterpret_cast<const float*>(E2), 2 * H, (long long)Nx * Ny * 2 * H, p.tz_e_big, p.tz_e_small,
+                    Nz, out, Nz, (long long)Nx * Ny * Nz, Nx * Ny, Nz, 2 * H, nf, s);
+  else
+    launch_sgemm(reinterpret_cast<const float*>(E2), 2 * H, (long long)Nx * Ny * 2 * H, p.tz_e, Nz, out, Nz,
+                 (long long)Nx * Ny * Nz, Nx * Ny, Nz, 2 * H, nf, s);
 }
 
 // project nf grid fields f[nf][N] -> half band G3[nf][Kx][Ky][H]
 void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, float2* G3, cudaStream_t s) {
   const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
   const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
-  launch_sgemm(f, Nz, (long long)Nx * Ny * Nz, p.tz_p, 2 * H, reinterpret_cast<float*>(G1), 2 * H,
-               (long long)Nx * Ny * 2 * H, Nx * Ny, 2 * H, Nz, nf, s);
+  if (use_tensor_cores())
+    launch_tc3_gemm(f, Nz, (long long)Nx * Ny * Nz, p.tz_p_big, p.tz_p_small, 2 * H, reinterpret_cast<float*>(G1),
+                    2 * H, (long long)Nx * Ny * 2 * H, Nx * Ny, 2 * H, Nz, nf, s);
+  else
+    launch_sgemm(f, Nz, (long long)Nx * Ny * Nz, p.tz_p, 2 * H, reinterpret_cast<float*>(G1), 2 * H,
+                 (long long)Nx * Ny * 2 * H, Nx * Ny, 2 * H, Nz, nf, s);
   launch_cgemm(p.wx_p, Nx, G1, (long long)Nx * Ny * H, Ny * H, G2, (long long)Kx * Ny * H, Ny * H, Kx, Ny * H,
                Nx, nf, s);
   launch_cgemm(p.wy_p, Ny, G2, (long long)Ny * H, H, G3, (long long)Ky * H, H, Ky, H, Ny, nf * Kx, s);
