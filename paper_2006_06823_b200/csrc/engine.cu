@@ -52,7 +52,7 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   }
   shape_require(p.nt >= 1, "nt must be >= 1");
   shape_require(p.alpha > 0.0 && p.s >= 1, "sobolev: alpha > 0 and s >= 1 required");
-  shape_require(p.variant == 2, "variant not supported by this engine build (deformation_state_equation only)");
+  shape_require(p.variant >= 0 && p.variant <= 2, "unknown variant");
   shape_require(p.stationary == 1, "nonstationary parameterization not supported by this engine build");
   LDDMM_CUDA(cudaSetDevice(device));
   LDDMM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -123,6 +123,8 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   dker_.alloc(3 * 1024);
   shape_require(p.dims[0] <= 1024 && p.dims[1] <= 1024 && p.dims[2] <= 1024, "grid dims must be <= 1024");
   opt_ws_.alloc(9 * vel_elems());
+  if (p.variant == 0) m0_.alloc(kprod());
+  ensure_variant_buffers();
 }
 
 Engine::~Engine() {
@@ -301,6 +303,17 @@ void Engine::set_images_impl(const double* I0d) {
     launch_circulant_axis_f64(I0d, g, dker_.p + 1024 * a, a, full_.N, stream_);
     launch_prefilter3d(g, full_.N, stream_);
     launch_f64_to_f32(N, g, I0coef_.p + (a + 1) * N, stream_);
+  }
+  // variant constants: m0 = pi(I0) (original, variants.hpp:374); spline coefficients of
+  // filtered_gradient(I0) = iota(grad pi(I0)) (state, variants.hpp:176-178,421)
+  if (prob_.variant == 0) project(I0, 1, m0_.p);
+  if (prob_.variant == 1) {
+    double2* pI0 = bt(11);
+    project(I0, 1, pI0);
+    PrepArgs pa{};
+    pa.nf = 3;
+    for (int a = 0; a < 3; ++a) pa.f[a] = PrepField{pI0, (SYM_DERIV_X + a) | SYM_PREFILTER, 1.0};
+    embed_fields(full_, pa, fgI0coef_.p, D_.p, E1_.p, E2_.p);
   }
   // mse denominator l2_inner(I0 - I1) (optimizer.hpp:151-154)
   {
@@ -658,10 +671,16 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
   provider_build(v, prov_, with_adjoint);
   Energies e;
   e.cfl = prov_.cfl;
-  solve_displacement_fwd(prov_, u_.p, true, nullptr);
   double ss = 0.0;
-  warp_m1(u_.p + prob_.nt * V, m1_.p, res_.p, with_adjoint, &ss);
-  if (with_adjoint) {
+  if (prob_.variant == 0) {
+    ss = forward_original(with_adjoint, v);
+  } else if (prob_.variant == 1) {
+    ss = forward_state(with_adjoint);
+  } else {
+    solve_displacement_fwd(prov_, u_.p, true, nullptr);
+    warp_m1(u_.p + prob_.nt * V, m1_.p, res_.p, with_adjoint, &ss);
+  }
+  if (with_adjoint && prob_.variant == 2) {
     float* gsw = m1_.p + N;
     launch_scale_vec(N, res_.p, -2.0 / prob_.sigma2, gsw, gridB_.p, stream_);  // r1
     double2* r1 = bt(10);
@@ -678,6 +697,7 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
 }
 
 double Engine::energy(const double2* v) {
+  if (prob_.variant == 0) return energy_original(v);
   provider_build(v, trial_prov_, false);
   solve_displacement_fwd(trial_prov_, nullptr, false, bt(11));
   double ss = 0.0;
@@ -688,11 +708,16 @@ double Engine::energy(const double2* v) {
 
 void Engine::gradient(double2* out) {
   shape_require(have_cache_ && cache_adjoint_, "gradient requires an adjoint-enabled forward cache");
-  assemble_jacT_terms(u_.p, rho_.p, prov_.v.p, out);
+  if (prob_.variant == 2)
+    assemble_jacT_terms(u_.p, rho_.p, prov_.v.p, out);
+  else
+    assemble_star_grad(lam_ser_.p, m_ser_.p, prov_.v.p, out);
 }
 
 void Engine::hessvec(const double2* dv, double2* out) {
   shape_require(have_cache_ && cache_adjoint_, "hessvec requires an adjoint-enabled forward cache");
+  if (prob_.variant == 0) return hessvec_original(dv, out);
+  if (prob_.variant == 1) return hessvec_state(dv, out);
   const long long V = vec_elems(), N = npts();
   const int nt = prob_.nt;
   DevBuf<double2>& series = dseries_;  // du series, then reused for the drho series
@@ -748,25 +773,7 @@ void Engine::maps(const double2* v, float* disp_fwd, float* disp_inv, double jac
   // u(1): forward displacement; nu(0): backward displacement (same SL scheme, src = v)
   double2* u1 = bt(11);
   solve_displacement_fwd(prov_, u_.p, true, u1);
-  // backward: mirror of solve_displacement_fwd with dep_bwd and sdt = -dt
-  double2* F = bt(0);
-  advect(prov_.v.p, 3, prov_.dep_bwd.p, F);
-  double2* prev = nullptr;
-  for (int s = 0; s < nt; ++s) {
-    double2* dst = rho_.p + (nt - s - 1) * V;
-    double2* tmp = bt(1);
-    if (s == 0) {
-      launch_scale(V, -0.5 * dt, prov_.v.p, tmp, stream_);
-    } else {
-      const double2* in[3] = {prev, prev + K, prev + 2 * K};
-      FinField outs[3];
-      for (int c = 0; c < 3; ++c) outs[c] = FinField{tmp + c * K, 1.0, prov_.v.p + c * K, -0.5 * dt};
-      advect_multi(in, 3, prov_.dep_bwd.p, outs);
-    }
-    launch_axpy(V, -0.5 * dt, F, tmp, dst, stream_);
-    prev = dst;
-  }
-  check_series_finite(rho_.p, nt, 0, true);
+  solve_displacement(prov_, false, rho_.p);
   const double2* nu0 = rho_.p;
   for (int which = 0; which < 2; ++which) {
     const double2* d = which == 0 ? u1 : nu0;

@@ -179,6 +179,17 @@ class Engine {
   DevBuf<double2> btmp_;      // band temporaries: 12 band vectors
   DevBuf<double2> src_;       // (nt+1) band vectors (incremental sources)
   DevBuf<double2> dseries_;   // (nt+1) band vectors (hessvec du / drho series)
+  // original / state_equation caches (variants.hpp:203-217), allocated on first use
+  DevBuf<double2> m_ser_;     // image state m_i (original) / reconstructed m_i (state), band scalars
+  DevBuf<double2> lam_ser_;   // lambda_i (original) / lambda nodes (state), band scalars
+  DevBuf<double2> dm_ser_;    // hessvec incremental scalar series (dm, dlambda)
+  DevBuf<double2> nu_ser_;    // state: nu series (band vectors)
+  DevBuf<double2> bigU_ser_;  // state: U series (band scalars)
+  DevBuf<float> jac_f_;       // state: J_i = 1 - iota(U_i), [nt+1][N]
+  DevBuf<float> psi_f_;       // state: iota(nu_i) displacement, [nt+1][3][N]
+  DevBuf<float> fgI0coef_;    // state: spline coefficients of filtered_gradient(I0), [3][N]
+  DevBuf<float> lcoef_;       // state: spline coefficients of lambda1 / dlambda1, [N]
+  DevBuf<double2> m0_;        // original: pi(I0)
   DevBuf<double> f64a_, f64b_, f64c_, dker_;  // fp64 grid scratch (image constants), derivative kernels
   DevBuf<float> maps_du_;     // 9 derivative fields for the Jacobian (allocated on first use)
   DevBuf<double2> opt_ws_;    // optimizer workspace: 9 velocities
@@ -193,6 +204,22 @@ class Engine {
   void solve_vector_continuity_bwd(ProviderState& ps, const double2* q1, double2* series);
   void solve_incremental_displacement(ProviderState& ps, const double2* dv, double2* series);
   void warp_m1(const double2* u1, float* m1, float* res, bool want_gsw, double* data_sumsq);
+  // variants.cu: original and state_equation (variants.hpp:373-422,444-527)
+  void ensure_variant_buffers();
+  void solve_displacement(ProviderState& ps, bool forward, double2* series);
+  void solve_image_forward(ProviderState& ps, const double2* m0, double2* series, bool keep_all, double2* last);
+  void solve_scalar_continuity_bwd(ProviderState& ps, const double2* q1, double2* series, bool jacobian_factor);
+  void solve_incremental_image(ProviderState& ps, const double2* dv, double2* series);
+  void small_custom(const PrepArgs& pa, int prodop, double2* out, int nout, double alpha, const double2* add,
+                    double beta);
+  void assemble_star_grad(const double2* Lam, const double2* Mser, const double2* like, double2* out);
+  void grid_spline(const float* f, float* coef);
+  void lambda_nodes_state(const float* lam1, double2* out_series);
+  double forward_original(bool with_adjoint, const double2* v);
+  double forward_state(bool with_adjoint);
+  double energy_original(const double2* v);
+  void hessvec_original(const double2* dv, double2* out);
+  void hessvec_state(const double2* dv, double2* out);
   void assemble_jacT_terms(const double2* series_u, const double2* series_q, const double2* like,
                            double2* out);
   void check_series_finite(const double2* series, int count, int first_step_offset, bool backward);

@@ -128,6 +128,8 @@ int launch_absmax_partial(long long n, const float* x, double* part, cudaStream_
 void launch_scale_vec(long long n, const float* res, double c, const float* g, float* out, cudaStream_t s);
 // dr1_a = ((-1 * sum_b g_b du_b) * c) * g_a   (variants.hpp:326-336)
 void launch_dr1(long long n, const float* g, const float* du, double c, float* out, cudaStream_t s);
+// dlam1 = ((-1 * sum_b g_b du_b) * c)   (variants.hpp:326-327)
+void launch_dlam1(long long n, const float* g, const float* du, double c, float* out, cudaStream_t s);
 // product kernels on the small grid, accumulate with weight w: op 0 jac, 1 jacT, 2 s*vec, 3 dot, 4 s*s
 void launch_products(int op, long long n, const float* a, const float* b, float* acc, float w, bool init,
                      cudaStream_t s);

@@ -112,6 +112,22 @@ void launch_dr1(long long n, const float* g, const float* du, double c, float* o
   LDDMM_LAUNCH_CHECK();
 }
 
+// dlam1 = ((-1 * sum_b g_b du_b) * c)   (variants.hpp:326-327, state branch)
+__global__ void dlam1_kernel(long long n, const float* __restrict__ g, const float* __restrict__ du, float c,
+                             float* __restrict__ out) {
+  GRID_STRIDE(i, n) {
+    float dm = 0.f;
+    dm += g[i] * du[i];
+    dm += g[n + i] * du[n + i];
+    dm += g[2 * n + i] * du[2 * n + i];
+    out[i] = (-dm) * c;
+  }
+}
+void launch_dlam1(long long n, const float* g, const float* du, double c, float* out, cudaStream_t s) {
+  dlam1_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, g, du, (float)c, out);
+  LDDMM_LAUNCH_CHECK();
+}
+
 // a: derivative fields / scalars, b: factors; layouts:
 //  op 0 jac : a = D[a][b][n] (d_b u_a), b = w[b][n] -> acc[a] += sum_b D[a][b] w[b]
 //  op 1 jacT: a = D[a][b][n],           b = w[a][n] -> acc[b] += sum_a D[a][b] w[a]

@@ -44,22 +44,25 @@ SETUPS = [
 ]
 
 
-def build(setup):
+VARIANTS = ["deformation_state_equation", "original", "state_equation"]
+
+
+def build(setup, variant="deformation_state_equation"):
     from paper_2006_06823_b200 import lddmm as L
     dims, band = setup["dims"], setup["band"]
     I0, I1 = smooth_pair(dims, 3)
     g = O.Grid(dims, (1.0, 1.0, 1.0))
     b = O.Band(g, band)
-    om = O.Model(b, I0, I1, "deformation_state_equation", setup["nt"], setup["sigma2"])
-    gm = L.Model(L.BandSpec(L.GridSpec(dims), band), I0, I1, "deformation_state_equation", setup["nt"],
-                 setup["sigma2"])
+    om = O.Model(b, I0, I1, variant, setup["nt"], setup["sigma2"])
+    gm = L.Model(L.BandSpec(L.GridSpec(dims), band), I0, I1, variant, setup["nt"], setup["sigma2"])
     return b, om, gm, I0, I1
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("setup", SETUPS)
-def test_forward_gradient_hessvec(cuda, setup):
-    """Model::forward / gradient / hessvec / precondition (variants.hpp:262-353)."""
-    b, om, gm, I0, I1 = build(setup)
+def test_forward_gradient_hessvec(cuda, setup, variant):
+    """Model::forward / gradient / hessvec / precondition for the three variants (variants.hpp:262-353)."""
+    b, om, gm, I0, I1 = build(setup, variant)
     v = rand_band(b, 21, 1.2)
     dv = rand_band(b, 22, 1.0)
     c = om.forward(v, True)
@@ -70,10 +73,12 @@ def test_forward_gradient_hessvec(cuda, setup):
     assert abs(e["cfl"] - c.cfl) <= 1e-5 * c.cfl
     m1, res = gm.fields()
     assert np.max(np.abs(m1 - c.m1)) < 1e-5
-    u = gm.series("u")
-    assert rel(u, np.stack(c.u)) < 1e-5
-    rho = gm.series("rho")
-    assert rel(rho, np.stack(c.rho)) < 1e-4
+    if variant != "original":
+        u = gm.series("u")
+        assert rel(u, np.stack(c.u)) < 1e-5
+    if variant == "deformation_state_equation":
+        rho = gm.series("rho")
+        assert rel(rho, np.stack(c.rho)) < 1e-4
     g_gpu = gm.gradient().numpy()[0]
     assert rel(g_gpu, om.gradient(c)) < 1e-4
     hv = gm.hessvec(gm.velocity(dv)).numpy()[0]
@@ -102,13 +107,13 @@ def test_hessian_symmetry_linearity(cuda):
     assert rel(hab, 2.0 * ha.numpy() + hb.numpy()) < 1e-5
 
 
-@pytest.mark.parametrize("fixed_work", [False, True])
-def test_optimize_matches_oracle(cuda, fixed_work):
+@pytest.mark.parametrize("variant,fixed_work", [(v, f) for v in VARIANTS for f in (False, True)])
+def test_optimize_matches_oracle(cuda, variant, fixed_work):
     """optimize (optimizer.hpp:143-262): same GN iterations, PCG iterations, step lengths and
-    stop reason; energies per iteration within 1e-5 relative."""
+    stop reason; energies per iteration within 1e-5 relative (config-3 style: every variant)."""
     from paper_2006_06823_b200 import lddmm as L
     setup = SETUPS[1]
-    b, om, gm, I0, I1 = build(setup)
+    b, om, gm, I0, I1 = build(setup, variant)
     kw = dict(max_iter=4)
     if fixed_work:
         kw.update(grad_tol=0.0, energy_tol=0.0, step_tol=0.0, pcg_tol=0.0, max_iter=3)
