@@ -271,9 +271,13 @@ class Context:
         self.nodes = 1 if parameterization == "stationary" else nt + 1
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().lddmm_destroy(self.h)
-            self.h = None
+        h = getattr(self, "h", None)
+        self.h = None
+        if h and _lib is not None:
+            try:
+                _lib.lddmm_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
 
     def check(self, rc, step=None):
         if rc != 0:
