@@ -53,7 +53,6 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   shape_require(p.nt >= 1, "nt must be >= 1");
   shape_require(p.alpha > 0.0 && p.s >= 1, "sobolev: alpha > 0 and s >= 1 required");
   shape_require(p.variant >= 0 && p.variant <= 2, "unknown variant");
-  shape_require(p.stationary == 1, "nonstationary parameterization not supported by this engine build");
   LDDMM_CUDA(cudaSetDevice(device));
   LDDMM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   double wunit[3];
@@ -97,12 +96,14 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   LDDMM_CUDA(cudaMallocHost(&host_slots_, (16 + 4096) * sizeof(double)));
 
   const long long V = vec_elems();
+  const int nsteps = p.stationary ? 1 : p.nt;  // departure slots per direction
   for (ProviderState* ps : {&prov_, &trial_prov_}) {
-    ps->v.alloc(V);
-    ps->div.alloc(kprod());
-    ps->dep_fwd.alloc(3 * N);
+    ps->v.alloc(nodes() * V);
+    ps->div.alloc(nodes() * kprod());
+    ps->dep_fwd.alloc(nsteps * 3 * N);
   }
-  prov_.dep_bwd.alloc(3 * N);
+  prov_.dep_bwd.alloc(nsteps * 3 * N);
+  if (!p.stationary) pscratch_.alloc(9 * N);
   u_.alloc((p.nt + 1) * V);
   rho_.alloc((p.nt + 1) * V);
   src_.alloc((p.nt + 1) * V);
@@ -469,26 +470,51 @@ void Engine::advect(const double2* q, int ncomp, const float* dep, double2* out)
 // band divergence, departure points, cfl
 
 void Engine::provider_build(const double2* v, ProviderState& ps, bool with_bwd) {
-  const long long N = npts(), K = kprod();
-  LDDMM_CUDA(cudaMemcpyAsync(ps.v.p, v, vec_elems() * sizeof(double2), cudaMemcpyDeviceToDevice, stream_));
-  launch_band_divergence(v, ps.div.p, full_.K, full_.omega_unit, stream_);
-  PrepArgs pa{};
-  pa.nf = 6;
-  for (int c = 0; c < 3; ++c) {
-    pa.f[c] = PrepField{v + c * K, SYM_NONE, 1.0};
-    pa.f[3 + c] = PrepField{v + c * K, SYM_PREFILTER, 1.0};
+  const long long N = npts(), K = kprod(), V = vec_elems();
+  const int nn = nodes(), nt = prob_.nt;
+  const double dt = 1.0 / nt;
+  LDDMM_CUDA(cudaMemcpyAsync(ps.v.p, v, vel_elems() * sizeof(double2), cudaMemcpyDeviceToDevice, stream_));
+  for (int i = 0; i < nn; ++i) launch_band_divergence(v + i * V, ps.div.p + i * K, full_.K, full_.omega_unit, stream_);
+  // per node: spatial node iota(v_i) and its spline coefficients iota(v_i / B)
+  auto embed_node = [&](int i, float* dst) {
+    PrepArgs pa{};
+    pa.nf = 6;
+    for (int c = 0; c < 3; ++c) {
+      pa.f[c] = PrepField{v + i * V + c * K, SYM_NONE, 1.0};
+      pa.f[3 + c] = PrepField{v + i * V + c * K, SYM_PREFILTER, 1.0};
+    }
+    embed_fields(full_, pa, dst, D_.p, E1_.p, E2_.p);
+    const int g = launch_absmax_partial(3 * N, dst, part_.p, stream_);
+    launch_reduce_final(part_, g, 1, slots_.p + 16 + i, stream_);  // cfl: max over nodes (transport.hpp:189-194)
+  };
+  if (prob_.stationary) {
+    embed_node(0, gridA_.p);
+    launch_departure(gridA_.p, gridA_.p + 3 * N, dt, h_, ps.dep_fwd.p, with_bwd ? ps.dep_bwd.p : nullptr, gridB_.p,
+                     full_.N, stream_);
+  } else {
+    // departure(step): forward from v_grid = node(step+1), v_traced = node(step); backward from
+    // v_grid = node(step), v_traced = node(step+1) (transport.hpp:176-187)
+    float* prev = pscratch_.p;         // grid + coefficients of node i-1 [6][N]
+    float* vm = pscratch_.p + 6 * N;   // gathered traced velocity [3][N]
+    for (int i = 0; i <= nt; ++i) {
+      embed_node(i, gridA_.p);
+      if (i >= 1) {
+        launch_departure_dir(gridA_.p, prev + 3 * N, dt, h_, -1.f, ps.dep_fwd.p + (i - 1) * 3 * N, vm, full_.N,
+                             stream_);
+        if (with_bwd)
+          launch_departure_dir(prev, gridA_.p + 3 * N, dt, h_, 1.f, ps.dep_bwd.p + (i - 1) * 3 * N, vm, full_.N,
+                               stream_);
+      }
+      LDDMM_CUDA(cudaMemcpyAsync(prev, gridA_.p, 6 * N * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+    }
   }
-  embed_fields(full_, pa, gridA_.p, D_.p, E1_.p, E2_.p);
-  const int g = launch_absmax_partial(3 * N, gridA_.p, part_.p, stream_);
-  launch_reduce_final(part_, g, 1, slots_.p + 1, stream_);
-  const double dt = 1.0 / prob_.nt;
-  launch_departure(gridA_.p, gridA_.p + 3 * N, dt, h_, ps.dep_fwd.p, with_bwd ? ps.dep_bwd.p : nullptr, gridB_.p,
-                   full_.N, stream_);
   ps.has_bwd = with_bwd;
-  LDDMM_CUDA(cudaMemcpyAsync(host_slots_ + 1, slots_.p + 1, sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  LDDMM_CUDA(cudaMemcpyAsync(host_slots_ + 16, slots_.p + 16, nn * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   sync();
+  double vmax = 0.0;
+  for (int i = 0; i < nn; ++i) vmax = std::max(vmax, host_slots_[16 + i]);
   const double hmin = std::min(h_[0], std::min(h_[1], h_[2]));
-  ps.cfl = host_slots_[1] * dt / hmin;
+  ps.cfl = vmax * dt / hmin;
 }
 
 void Engine::departure(const double2* v, float* dep_fwd, float* dep_bwd, double* cfl) {
@@ -536,20 +562,32 @@ void Engine::solve_displacement_fwd(ProviderState& ps, double2* series, bool kee
   const int nt = prob_.nt;
   const double dt = 1.0 / nt;
   double2* F = bt(0);
-  advect(ps.v.p, 3, ps.dep_fwd.p, F);
+  if (prob_.stationary) advect(ps.v.p, 3, ps.dep_fwd.p, F);
   double2* prev = nullptr;
   for (int s = 0; s < nt; ++s) {
     double2* dst = keep_all ? series + (s + 1) * V : tmp_u_.p + ((s + 1) & 1) * V;
     double2* tmp = bt(1);
-    if (s == 0) {
-      launch_scale(V, 0.5 * dt, ps.v.p, tmp, stream_);  // 0.5 dt v + 0
+    if (prob_.stationary) {
+      if (s == 0) {
+        launch_scale(V, 0.5 * dt, ps.v.p, tmp, stream_);  // 0.5 dt v + 0
+      } else {
+        const double2* in[3] = {prev, prev + K, prev + 2 * K};
+        FinField outs[3];
+        for (int c = 0; c < 3; ++c) outs[c] = FinField{tmp + c * K, 1.0, ps.v.p + c * K, 0.5 * dt};
+        advect_multi(in, 3, ps.dep_fwd.p, outs);
+      }
+      launch_axpy(V, 0.5 * dt, F, tmp, dst, stream_);
     } else {
-      const double2* in[3] = {prev, prev + K, prev + 2 * K};
+      // q-independent source v(t_i): merged advect, next = advect(u_s + dt/2 v_s) + dt/2 v_{s+1}
+      if (s == 0)
+        launch_scale(V, 0.5 * dt, vnode(ps, 0), tmp, stream_);
+      else
+        launch_axpy(V, 0.5 * dt, vnode(ps, s), prev, tmp, stream_);
+      const double2* in[3] = {tmp, tmp + K, tmp + 2 * K};
       FinField outs[3];
-      for (int c = 0; c < 3; ++c) outs[c] = FinField{tmp + c * K, 1.0, ps.v.p + c * K, 0.5 * dt};
-      advect_multi(in, 3, ps.dep_fwd.p, outs);
+      for (int c = 0; c < 3; ++c) outs[c] = FinField{dst + c * K, 1.0, vnode(ps, s + 1) + c * K, 0.5 * dt};
+      advect_multi(in, 3, depf(ps, s), outs);
     }
-    launch_axpy(V, 0.5 * dt, F, tmp, dst, stream_);
     enqueue_finite_check(dst, s);
     prev = dst;
   }
@@ -568,16 +606,16 @@ void Engine::solve_vector_continuity_bwd(ProviderState& ps, const double2* q1, d
     const int from = nt - s, to = nt - s - 1;
     const double2* q = series + from * V;
     double2 *sf = bt(0), *A = bt(1), *F = bt(2), *qs = bt(3), *ft = bt(4), *tmp = bt(5);
-    small_product(1, ps.div.p, q, sf, -1.0, nullptr, 0.0);  // src(q_from) = -(div * q)
+    small_product(1, divnode(ps, from), q, sf, -1.0, nullptr, 0.0);  // src(q_from) = -(div * q)
     const double2* in[6] = {q, q + K, q + 2 * K, sf, sf + K, sf + 2 * K};
     FinField outs[6];
     for (int c = 0; c < 3; ++c) {
       outs[c] = FinField{A + c * K, 1.0, nullptr, 0.0};
       outs[3 + c] = FinField{F + c * K, 1.0, nullptr, 0.0};
     }
-    advect_multi(in, 6, ps.dep_bwd.p, outs);
-    launch_axpy(V, sdt, F, A, qs, stream_);                   // q* = sdt f_from + A
-    small_product(1, ps.div.p, qs, ft, -1.0, nullptr, 0.0);  // f_to = src(q*)
+    advect_multi(in, 6, depb(ps, to), outs);
+    launch_axpy(V, sdt, F, A, qs, stream_);                          // q* = sdt f_from + A
+    small_product(1, divnode(ps, to), qs, ft, -1.0, nullptr, 0.0);  // f_to = src(q*)
     launch_axpy(V, 0.5 * sdt, ft, A, tmp, stream_);           // 0.5 sdt f_to + A
     launch_axpy(V, 0.5 * sdt, F, tmp, series + to * V, stream_);
   }
@@ -590,9 +628,10 @@ void Engine::solve_incremental_displacement(ProviderState& ps, const double2* dv
   const long long V = vec_elems(), K = kprod();
   const int nt = prob_.nt;
   const double dt = 1.0 / nt;
-  // sources src_i = -jac(u_i, dv) + dv ; u_0 = 0 so src_0 = dv exactly
+  // sources src_i = -jac(u_i, dv_i) + dv_i ; u_0 = 0 so src_0 = dv_0 exactly
   LDDMM_CUDA(cudaMemcpyAsync(src_.p, dv, V * sizeof(double2), cudaMemcpyDeviceToDevice, stream_));
-  for (int i = 1; i <= nt; ++i) small_product(3, u_.p + i * V, dv, src_.p + i * V, -1.0, dv, 1.0);
+  for (int i = 1; i <= nt; ++i)
+    small_product(3, u_.p + i * V, tvnode(dv, i), src_.p + i * V, -1.0, tvnode(dv, i), 1.0);
   LDDMM_CUDA(cudaMemsetAsync(series, 0, V * sizeof(double2), stream_));
   for (int s = 0; s < nt; ++s) {
     double2* in = bt(0);
@@ -601,7 +640,7 @@ void Engine::solve_incremental_displacement(ProviderState& ps, const double2* dv
     FinField outs[3];
     for (int c = 0; c < 3; ++c)
       outs[c] = FinField{series + (s + 1) * V + c * K, 1.0, src_.p + (s + 1) * V + c * K, 0.5 * dt};
-    advect_multi(ins, 3, ps.dep_fwd.p, outs);
+    advect_multi(ins, 3, depf(ps, s), outs);
   }
   check_series_finite(series, nt, 0, false);
 }
@@ -620,6 +659,20 @@ void Engine::assemble_jacT_terms(const double2* U, const double2* Q, const doubl
   const long long V = vec_elems(), K = kprod(), M = small_.npts();
   const int nt = prob_.nt;
   const auto w = trapezoid_weights(nt);
+  if (!prob_.stationary) {
+    // nonstationary: out_i = L like_i + (q_i - jacT(u_i, q_i)) (variants.hpp:364-368)
+    for (int i = 0; i <= nt; ++i) {
+      double2* tmp = bt(7);
+      if (i == 0)
+        LDDMM_CUDA(cudaMemcpyAsync(tmp, Q, V * sizeof(double2), cudaMemcpyDeviceToDevice, stream_));
+      else
+        small_product(4, U + i * V, Q + i * V, tmp, -1.0, Q + i * V, 1.0);
+      double2* lv = bt(8);
+      launch_sobolev(like + i * V, lv, 3, full_.K, full_.omega_unit, prob_.alpha, prob_.s, false, stream_);
+      launch_axpy(V, 1.0, lv, tmp, out + i * V, stream_);
+    }
+    return;
+  }
   // band part: acc = sum_i w_i q_i
   double2* acc = bt(6);
   launch_scale(V, w[0], Q, acc, stream_);
@@ -657,12 +710,19 @@ void Engine::assemble_jacT_terms(const double2* U, const double2* Q, const doubl
 // ---------------------------------------------------------------------------
 // Model API
 
-double Engine::reg_energy(const double2* v) {  // variants.hpp:280-281
-  double2* lv = bt(9);
-  launch_sobolev(v, lv, 3, full_.K, full_.omega_unit, prob_.alpha, prob_.s, false, stream_);
-  const int g = launch_inner_partial(vec_elems(), lv, v, part_.p, stream_);
-  const double s = reduce(g, 0);
-  return 0.5 * s * cell_volume_ / (double)npts();
+double Engine::reg_energy(const double2* v) {  // variants.hpp:280-287
+  const long long V = vec_elems();
+  const auto w = trapezoid_weights(prob_.nt);
+  double acc = 0.0;
+  for (int i = 0; i < nodes(); ++i) {
+    double2* lv = bt(9);
+    launch_sobolev(v + i * V, lv, 3, full_.K, full_.omega_unit, prob_.alpha, prob_.s, false, stream_);
+    const int g = launch_inner_partial(V, lv, v + i * V, part_.p, stream_);
+    const double s = reduce(g, 0) * cell_volume_ / (double)npts();
+    if (prob_.stationary) return 0.5 * s;
+    acc += w[i] * s;
+  }
+  return 0.5 * acc;
 }
 
 Energies Engine::forward(const double2* v, bool with_adjoint) {
@@ -738,9 +798,19 @@ void Engine::tv_axpy(double a, const double2* x, const double2* y, double2* out)
   launch_axpy(vel_elems(), a, x, y, out, stream_);
 }
 void Engine::tv_scaled(const double2* x, double a, double2* out) { launch_scale(vel_elems(), a, x, out, stream_); }
-double Engine::tv_inner(const double2* a, const double2* b) {
-  const int g = launch_inner_partial(vel_elems(), a, b, part_.p, stream_);
-  return reduce(g, 0) * cell_volume_ / (double)npts();
+double Engine::tv_inner(const double2* a, const double2* b) {  // variants.hpp:94-103
+  if (prob_.stationary) {
+    const int g = launch_inner_partial(vel_elems(), a, b, part_.p, stream_);
+    return reduce(g, 0) * cell_volume_ / (double)npts();
+  }
+  const long long V = vec_elems();
+  const auto w = trapezoid_weights(prob_.nt);
+  double s = 0.0;
+  for (int i = 0; i <= prob_.nt; ++i) {
+    const int g = launch_inner_partial(V, a + i * V, b + i * V, part_.p, stream_);
+    s += w[i] * (reduce(g, 0) * cell_volume_ / (double)npts());
+  }
+  return s;
 }
 double Engine::tv_linf(const double2* a) {
   const int g = launch_linf_partial(vel_elems(), a, part_.p, stream_);

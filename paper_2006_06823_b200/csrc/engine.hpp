@@ -197,6 +197,23 @@ class Engine {
   void build_plan(DftPlan& p, const int* Ngrid, const int* K, const double* parent_wunit);
   void free_plans();
   double2* bt(int i) const { return btmp_.p + (long long)i * vec_elems(); }
+  // per-node / per-step views (stationary: one slot, transport.hpp:124-130)
+  const float* depf(const ProviderState& ps, int step) const {
+    return ps.dep_fwd.p + (prob_.stationary ? 0 : (long long)step * 3 * npts());
+  }
+  const float* depb(const ProviderState& ps, int step) const {
+    return ps.dep_bwd.p + (prob_.stationary ? 0 : (long long)step * 3 * npts());
+  }
+  const double2* vnode(const ProviderState& ps, int i) const {
+    return ps.v.p + (prob_.stationary ? 0 : (long long)i * vec_elems());
+  }
+  const double2* divnode(const ProviderState& ps, int i) const {
+    return ps.div.p + (prob_.stationary ? 0 : (long long)i * kprod());
+  }
+  const double2* tvnode(const double2* tv, int i) const {  // tv_node (variants.hpp:65-68)
+    return tv + (prob_.stationary ? 0 : (long long)i * vec_elems());
+  }
+  DevBuf<float> pscratch_;  // nonstationary provider scratch [9][N]
   double2* node(DevBuf<double2>& s, int i) const { return s.p + (long long)i * vec_elems(); }
 
   void provider_build(const double2* v, ProviderState& ps, bool with_bwd);

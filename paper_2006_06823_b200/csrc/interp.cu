@@ -637,18 +637,19 @@ __global__ void departure_combine_kernel(long long n, const float* __restrict__ 
 // sl_departure (transport.hpp:83-102) for a stationary velocity: X* = x + sg dt v(x),
 // v_traced(X*) through the production gather (displacement scale sg dt / h), then the
 // trapezoid combination; scratch holds [3][N] floats per direction.
-void launch_departure(const float* vgrid, const float* vcoef, double dt, const double* h, float* dep_fwd,
-                      float* dep_bwd, float* scratch, const int* N, cudaStream_t s) {
+void launch_departure_dir(const float* vgrid, const float* vcoef, double dt, const double* h, float sg, float* out,
+                          float* vm, const int* N, cudaStream_t s) {
   const long long n = (long long)N[0] * N[1] * N[2];
   const float dtx = (float)(dt / h[0]), dty = (float)(dt / h[1]), dtz = (float)(dt / h[2]);
-  for (int dir = 0; dir < (dep_bwd ? 2 : 1); ++dir) {
-    const float sg = dir == 0 ? -1.f : 1.f;
-    float* vm = scratch + dir * 3 * n;
-    launch_gather_scaled(vcoef, 3, vgrid, sg * dtx, sg * dty, sg * dtz, vm, N, s);
-    departure_combine_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, vgrid, vm, dtx, dty, dtz, sg,
-                                                              dir == 0 ? dep_fwd : dep_bwd);
-    LDDMM_LAUNCH_CHECK();
-  }
+  launch_gather_scaled(vcoef, 3, vgrid, sg * dtx, sg * dty, sg * dtz, vm, N, s);
+  departure_combine_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, vgrid, vm, dtx, dty, dtz, sg, out);
+  LDDMM_LAUNCH_CHECK();
+}
+
+void launch_departure(const float* vgrid, const float* vcoef, double dt, const double* h, float* dep_fwd,
+                      float* dep_bwd, float* scratch, const int* N, cudaStream_t s) {
+  launch_departure_dir(vgrid, vcoef, dt, h, -1.f, dep_fwd, scratch, N, s);
+  if (dep_bwd) launch_departure_dir(vgrid, vcoef, dt, h, 1.f, dep_bwd, scratch, N, s);
 }
 
 // pull-back through points x - disp (disp physical): the production gather with

@@ -85,6 +85,10 @@ void launch_gather_cubic_global(const float* coef, int ncomp, const float* disp,
 // grid-unit departure displacements for both directions (transport.hpp:83-102)
 void launch_departure(const float* vgrid, const float* vcoef, double dt, const double* h, float* dep_fwd,
                       float* dep_bwd, float* scratch, const int* N, cudaStream_t s);
+// one direction: X* = x + sg dt vgrid, out = sg dt/2 (vcoef-sample(X*) + vgrid) in grid units;
+// vm: [3][N] scratch (separate arrival / traced nodes for nonstationary velocities)
+void launch_departure_dir(const float* vgrid, const float* vcoef, double dt, const double* h, float sg, float* out,
+                          float* vm, const int* N, cudaStream_t s);
 // gather with the displacement scaled per axis: samples coef at node + (sx dx, sy dy, sz dz)
 void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
                           const int* N, cudaStream_t s);

@@ -50,23 +50,33 @@ void Engine::solve_displacement(ProviderState& ps, bool forward, double2* series
   const long long V = vec_elems(), K = kprod();
   const int nt = prob_.nt;
   const double sdt = forward ? 1.0 / nt : -1.0 / nt;
-  const float* dep = forward ? ps.dep_fwd.p : ps.dep_bwd.p;
   double2* F = bt(0);
-  advect(ps.v.p, 3, dep, F);
+  if (prob_.stationary) advect(ps.v.p, 3, forward ? ps.dep_fwd.p : ps.dep_bwd.p, F);
   LDDMM_CUDA(cudaMemsetAsync(series + (forward ? 0 : nt) * V, 0, V * sizeof(double2), stream_));
   for (int s = 0; s < nt; ++s) {
     const int from = forward ? s : nt - s, to = forward ? s + 1 : nt - s - 1;
+    const int step = forward ? s : nt - s - 1;
+    const float* dep = forward ? depf(ps, step) : depb(ps, step);
     double2* tmp = bt(1);
-    if (s == 0) {
-      launch_scale(V, 0.5 * sdt, ps.v.p, tmp, stream_);
+    if (prob_.stationary) {
+      if (s == 0) {
+        launch_scale(V, 0.5 * sdt, ps.v.p, tmp, stream_);
+      } else {
+        const double2* q = series + from * V;
+        const double2* in[3] = {q, q + K, q + 2 * K};
+        FinField outs[3];
+        for (int c = 0; c < 3; ++c) outs[c] = FinField{tmp + c * K, 1.0, ps.v.p + c * K, 0.5 * sdt};
+        advect_multi(in, 3, dep, outs);
+      }
+      launch_axpy(V, 0.5 * sdt, F, tmp, series + to * V, stream_);
     } else {
-      const double2* q = series + from * V;
-      const double2* in[3] = {q, q + K, q + 2 * K};
+      launch_axpy(V, 0.5 * sdt, vnode(ps, from), series + from * V, tmp, stream_);
+      const double2* in[3] = {tmp, tmp + K, tmp + 2 * K};
       FinField outs[3];
-      for (int c = 0; c < 3; ++c) outs[c] = FinField{tmp + c * K, 1.0, ps.v.p + c * K, 0.5 * sdt};
+      for (int c = 0; c < 3; ++c)
+        outs[c] = FinField{series + to * V + c * K, 1.0, vnode(ps, to) + c * K, 0.5 * sdt};
       advect_multi(in, 3, dep, outs);
     }
-    launch_axpy(V, 0.5 * sdt, F, tmp, series + to * V, stream_);
     enqueue_finite_check(series + to * V, s);
   }
   finish_finite_checks(nt);
@@ -84,7 +94,7 @@ void Engine::solve_image_forward(ProviderState& ps, const double2* m0, double2* 
     double2* dst = keep_all ? series + (s + 1) * S : tmp_u_.p + ((s + 1) & 1) * S;
     const double2* in[1] = {prev};
     FinField outs[1] = {FinField{dst, 1.0, nullptr, 0.0}};
-    advect_multi(in, 1, ps.dep_fwd.p, outs);
+    advect_multi(in, 1, depf(ps, s), outs);
     // the finite check reads a vector-sized block; scalars use their own length
     const int g = launch_nonfinite_partial(S, dst, part2_.p, stream_);
     launch_reduce_final(part2_.p, g, 1, slots_.p + 16 + s, stream_);
@@ -104,17 +114,16 @@ void Engine::solve_scalar_continuity_bwd(ProviderState& ps, const double2* q1, d
     LDDMM_CUDA(cudaMemcpyAsync(series + nt * S, q1, S * sizeof(double2), cudaMemcpyDeviceToDevice, stream_));
   else
     LDDMM_CUDA(cudaMemsetAsync(series + nt * S, 0, S * sizeof(double2), stream_));
-  const double2* add = jf ? ps.div.p : nullptr;
   for (int s = 0; s < nt; ++s) {
     const int from = nt - s, to = nt - s - 1;
     const double2* q = series + from * S;
     double2 *sf = bt(0), *A = bt(1), *F = bt(2), *qs = bt(3), *ft = bt(4), *tmp = bt(5);
-    small_product(0, q, ps.div.p, sf, -1.0, add, 1.0);  // src(q_from)
+    small_product(0, q, divnode(ps, from), sf, -1.0, jf ? divnode(ps, from) : nullptr, 1.0);  // src(q_from)
     const double2* in[2] = {q, sf};
     FinField outs[2] = {FinField{A, 1.0, nullptr, 0.0}, FinField{F, 1.0, nullptr, 0.0}};
-    advect_multi(in, 2, ps.dep_bwd.p, outs);
+    advect_multi(in, 2, depb(ps, to), outs);
     launch_axpy(S, sdt, F, A, qs, stream_);
-    small_product(0, qs, ps.div.p, ft, -1.0, add, 1.0);  // src(q*)
+    small_product(0, qs, divnode(ps, to), ft, -1.0, jf ? divnode(ps, to) : nullptr, 1.0);  // src(q*)
     launch_axpy(S, 0.5 * sdt, ft, A, tmp, stream_);
     launch_axpy(S, 0.5 * sdt, F, tmp, series + to * S, stream_);
     const int g = launch_nonfinite_partial(S, series + to * S, part2_.p, stream_);
@@ -147,8 +156,8 @@ void Engine::solve_incremental_image(ProviderState& ps, const double2* dv, doubl
     PrepArgs pa{};
     pa.nf = 6;
     for (int a = 0; a < 3; ++a) pa.f[a] = PrepField{m_ser_.p + i * S, SYM_DERIV_X + a, 1.0};
-    for (int c = 0; c < 3; ++c) pa.f[3 + c] = PrepField{dv + c * K, SYM_NONE, 1.0};
-    small_custom(pa, 3, src + i * S, 1, -1.0, nullptr, 0.0);  // -star_dot(grad m_i, dv)
+    for (int c = 0; c < 3; ++c) pa.f[3 + c] = PrepField{tvnode(dv, i) + c * K, SYM_NONE, 1.0};
+    small_custom(pa, 3, src + i * S, 1, -1.0, nullptr, 0.0);  // -star_dot(grad m_i, dv_i)
   }
   LDDMM_CUDA(cudaMemsetAsync(series, 0, S * sizeof(double2), stream_));
   for (int s = 0; s < nt; ++s) {
@@ -156,7 +165,7 @@ void Engine::solve_incremental_image(ProviderState& ps, const double2* dv, doubl
     launch_axpy(S, 0.5 * dt, src + s * S, series + s * S, in, stream_);
     const double2* ins[1] = {in};
     FinField outs[1] = {FinField{series + (s + 1) * S, 1.0, src + (s + 1) * S, 0.5 * dt}};
-    advect_multi(ins, 1, ps.dep_fwd.p, outs);
+    advect_multi(ins, 1, depf(ps, s), outs);
     const int g = launch_nonfinite_partial(S, series + (s + 1) * S, part2_.p, stream_);
     launch_reduce_final(part2_.p, g, 1, slots_.p + 16 + s, stream_);
   }
@@ -168,6 +177,20 @@ void Engine::assemble_star_grad(const double2* Lam, const double2* Mser, const d
   const long long S = kprod(), V = vec_elems(), M = small_.npts(), K = kprod();
   const int nt = prob_.nt;
   const auto w = trap_w(nt);
+  if (!prob_.stationary) {  // out_i = L like_i + star(Lam_i, grad M_i)  (variants.hpp:364-368)
+    for (int i = 0; i <= nt; ++i) {
+      PrepArgs pa{};
+      pa.nf = 4;
+      pa.f[0] = PrepField{Lam + i * S, SYM_NONE, 1.0};
+      for (int a = 0; a < 3; ++a) pa.f[1 + a] = PrepField{Mser + i * S, SYM_DERIV_X + a, 1.0};
+      double2* tmp = bt(7);
+      small_custom(pa, 2, tmp, 3, 1.0, nullptr, 0.0);
+      double2* lv = bt(8);
+      launch_sobolev(like + i * V, lv, 3, full_.K, full_.omega_unit, prob_.alpha, prob_.s, false, stream_);
+      launch_axpy(V, 1.0, lv, tmp, out + i * V, stream_);
+    }
+    return;
+  }
   for (int i = 0; i <= nt; ++i) {
     PrepArgs pa{};
     pa.nf = 4;

@@ -112,6 +112,27 @@ def optimize():
     np.savez_compressed(os.path.join(HERE, "optimize.npz"), **out)
 
 
+def model_nonstationary():
+    """Nonstationary parameterization (core.hpp:290-316; transport.hpp:120-131,176-187;
+    variants.hpp:364-368): forward/gradient/hessvec of the three variants + a short optimize."""
+    dims, h, band, nt = (16, 12, 14), (1.0, 1.0, 1.0), (8, 8, 6), 3
+    I0 = ref.random_smooth_image(dims, h, 61, 1.0)
+    I1 = ref.random_smooth_image(dims, h, 62, 1.0)
+    v = np.stack([ref.random_band_field(dims, h, band, 63 + i, 1.0, 2.0) for i in range(nt + 1)])
+    dv = np.stack([ref.random_band_field(dims, h, band, 73 + i, 1.0, 2.0) for i in range(nt + 1)])
+    out = dict(dims=np.array(dims), band=np.array(band), nt=nt, sigma2=0.5, I0=I0, I1=I1, v=v, dv=dv)
+    for var in ("deformation_state_equation", "original", "state_equation"):
+        m = ref.RefModel(I0, I1, dims, h, band, var, nt, 0.5, param="nonstationary")
+        e = m.forward(v, True)
+        out[f"{var}_energy"] = np.array([e["energy"], e["energy_reg"], e["energy_data"], e["cfl"]])
+        out[f"{var}_gradient"] = m.gradient()
+        out[f"{var}_hessvec"] = m.hessvec(dv)
+        r = m.optimize(None, max_iter=3)
+        out[f"{var}_opt_history"] = np.array([[q.iter, q.energy, q.pcg_iters, q.epsilon] for q in r["history"]])
+        out[f"{var}_opt_stop"] = ref.STOP_REASONS.index(r["stop"])
+    np.savez_compressed(os.path.join(HERE, "model_ns.npz"), **out)
+
+
 if __name__ == "__main__":
     if not ref.available():
         sys.exit("build oracle/_ref first: make -C oracle ref")
@@ -120,6 +141,7 @@ if __name__ == "__main__":
     transport()
     model()
     optimize()
+    model_nonstationary()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -152,3 +152,34 @@ def test_divergence_reported(cuda):
     v[0, 1, 1, 1] = np.nan
     with pytest.raises(L.DivergenceError):
         gm.forward(gm.velocity(v), True)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_nonstationary_model_and_optimize(cuda, variant):
+    """Nonstationary parameterization on the device vs the oracle: forward / gradient /
+    hessvec and a short optimize with identical GN/PCG path (core.hpp:290-316,
+    transport.hpp:120-187, variants.hpp:364-368)."""
+    from paper_2006_06823_b200 import lddmm as L
+    setup = SETUPS[0]
+    dims, band, nt = setup["dims"], setup["band"], setup["nt"]
+    I0, I1 = smooth_pair(dims, 3)
+    g = O.Grid(dims, (1.0, 1.0, 1.0))
+    b = O.Band(g, band)
+    om = O.Model(b, I0, I1, variant, nt, setup["sigma2"], stationary=False)
+    gm = L.Model(L.BandSpec(L.GridSpec(dims), band), I0, I1, variant, nt, setup["sigma2"],
+                 parameterization="nonstationary")
+    v = [rand_band(b, 90 + i, 1.0) for i in range(nt + 1)]
+    dv = [rand_band(b, 95 + i, 1.0) for i in range(nt + 1)]
+    c = om.forward(v, True)
+    e = gm.forward(gm.velocity(np.stack(v)), True)
+    assert abs(e["energy"] - c.energy) <= 1e-5 * abs(c.energy)
+    assert abs(e["cfl"] - c.cfl) <= 1e-5 * c.cfl
+    assert rel(gm.gradient().numpy(), np.stack(om.gradient(c))) < 1e-4
+    assert rel(gm.hessvec(gm.velocity(np.stack(dv))).numpy(), np.stack(om.hessvec(c, dv))) < 1e-4
+    ref = O.optimize(om, om.zero_velocity(), O.Options(max_iter=3))
+    res = L.optimize(gm, None, L.OptimizeOptions(max_iter=3))
+    assert res.stop == ref["stop"] and res.iterations == ref["iterations"]
+    for r, q in zip(res.history, ref["history"]):
+        assert r.pcg_iters == q["pcg_iters"] and r.epsilon == q["epsilon"]
+        assert abs(r.energy - q["energy"]) <= 1e-5 * abs(q["energy"])
+    assert rel(res.v.numpy(), np.stack(ref["v"])) < 1e-4

@@ -161,3 +161,28 @@ def test_unit_kats():
     rng = np.random.default_rng(2)
     h = rng.standard_normal(g.dims)
     assert np.max(np.abs(O.warp(h, x, g, "cubic") - h)) < 1e-12
+
+
+@pytest.mark.parametrize("variant", ["deformation_state_equation", "original", "state_equation"])
+def test_model_nonstationary_golden(variant):
+    """Nonstationary parameterization: per-node providers, departures per step, per-node
+    assembly and trapezoid-weighted inner products (core.hpp:290-316, transport.hpp:120-187,
+    variants.hpp:94-103,280-287,364-368)."""
+    z = load("model_ns")
+    dims = tuple(int(x) for x in z["dims"])
+    g = O.Grid(dims, (1.0, 1.0, 1.0))
+    b = O.Band(g, tuple(int(x) for x in z["band"]))
+    nt = int(z["nt"])
+    m = O.Model(b, z["I0"], z["I1"], variant, nt, float(z["sigma2"]), stationary=False)
+    v, dv = list(z["v"]), list(z["dv"])
+    c = m.forward(v, True)
+    assert np.allclose([c.energy, c.energy_reg, c.energy_data, c.cfl], z[f"{variant}_energy"], rtol=1e-12)
+    assert rel(np.stack(m.gradient(c)), z[f"{variant}_gradient"]) < 1e-11
+    assert rel(np.stack(m.hessvec(c, dv)), z[f"{variant}_hessvec"]) < 1e-11
+    r = O.optimize(m, m.zero_velocity(), O.Options(max_iter=3))
+    hist = z[f"{variant}_opt_history"]
+    assert O.STOP.index(r["stop"]) == int(z[f"{variant}_opt_stop"])
+    assert len(r["history"]) == hist.shape[0]
+    for q, row in zip(r["history"], hist):
+        assert q["pcg_iters"] == int(row[2]) and q["epsilon"] == row[3]
+        assert abs(q["energy"] - row[1]) <= 1e-9 * abs(row[1])
