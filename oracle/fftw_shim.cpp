@@ -54,10 +54,9 @@ struct Plan1D {
     if (p > 64) { big.resize(p); tp = big.data(); }
     const int nn = n;
     for (int k = 0; k < m; ++k) {
-      for (int r = 0; r < p; ++r) {
-        long e = (long)r * k * ws % nn;
-        tp[r] = out[r * m + k] * w[e];
-      }
+      tp[0] = out[k];
+      for (int r = 1; r < p; ++r) tp[r] = out[r * m + k] * w[(long)r * k * ws];  // r k ws < n
+
       if (p == 2) {
         out[k] = tp[0] + tp[1];
         out[k + m] = tp[0] - tp[1];
@@ -127,24 +126,45 @@ void fftw_execute_dft(const fftw_plan p, fftw_complex* in_, fftw_complex* out_) 
     const std::size_t outer = total / ((std::size_t)n * stride);
     const std::size_t lines = outer * stride;
     const Plan1D& pl = *p->axes[a];
-    auto work = [&](std::size_t l0, std::size_t l1) {
+    // Lines along a strided axis are processed in blocks of B neighbouring lines
+    // (contiguous in memory): the block is copied with B-element row copies,
+    // each column transformed, and copied back -- cache-friendly for the slow axes.
+    constexpr std::size_t B = 16;
+    const std::size_t nblk_per_outer = stride >= B ? (stride + B - 1) / B : stride;
+    const bool blocked = stride >= B;
+    const std::size_t units = blocked ? outer * nblk_per_outer : lines;
+    auto work = [&](std::size_t u0, std::size_t u1) {
       std::vector<cplx> a_(n), b_(n);
-      for (std::size_t l = l0; l < l1; ++l) {
-        const std::size_t o = l / stride, s = l % stride;
-        cplx* base = out + o * (std::size_t)n * stride + s;
-        for (int k = 0; k < n; ++k) a_[k] = base[(std::size_t)k * stride];
-        pl.exec(a_.data(), b_.data());
-        for (int k = 0; k < n; ++k) base[(std::size_t)k * stride] = b_[k];
+      std::vector<cplx> blk(blocked ? (std::size_t)n * B : 0);
+      for (std::size_t u = u0; u < u1; ++u) {
+        if (!blocked) {
+          const std::size_t o = u / stride, s = u % stride;
+          cplx* base = out + o * (std::size_t)n * stride + s;
+          for (int k = 0; k < n; ++k) a_[k] = base[(std::size_t)k * stride];
+          pl.exec(a_.data(), b_.data());
+          for (int k = 0; k < n; ++k) base[(std::size_t)k * stride] = b_[k];
+          continue;
+        }
+        const std::size_t o = u / nblk_per_outer, s0 = (u % nblk_per_outer) * B;
+        const std::size_t w = std::min(B, stride - s0);
+        cplx* base = out + o * (std::size_t)n * stride + s0;
+        for (int k = 0; k < n; ++k) std::memcpy(&blk[(std::size_t)k * B], base + (std::size_t)k * stride, w * sizeof(cplx));
+        for (std::size_t j = 0; j < w; ++j) {
+          for (int k = 0; k < n; ++k) a_[k] = blk[(std::size_t)k * B + j];
+          pl.exec(a_.data(), b_.data());
+          for (int k = 0; k < n; ++k) blk[(std::size_t)k * B + j] = b_[k];
+        }
+        for (int k = 0; k < n; ++k) std::memcpy(base + (std::size_t)k * stride, &blk[(std::size_t)k * B], w * sizeof(cplx));
       }
     };
-    const int nth = (int)std::min<std::size_t>((std::size_t)g_threads, lines);
+    const int nth = (int)std::min<std::size_t>((std::size_t)g_threads, units);
     if (nth <= 1 || total < 32768) {
-      work(0, lines);
+      work(0, units);
     } else {
       std::vector<std::thread> th;
-      const std::size_t chunk = (lines + nth - 1) / nth;
+      const std::size_t chunk = (units + nth - 1) / nth;
       for (int t = 0; t < nth; ++t) {
-        std::size_t l0 = t * chunk, l1 = std::min(lines, l0 + chunk);
+        std::size_t l0 = t * chunk, l1 = std::min(units, l0 + chunk);
         if (l0 < l1) th.emplace_back(work, l0, l1);
       }
       for (auto& x : th) x.join();

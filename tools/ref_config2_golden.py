@@ -2,7 +2,7 @@
 offline, and store its GN-Krylov history and final velocity as a golden fixture
 (tests/golden/config2_ref.npz).  Takes O(hours) of CPU; run in this container:
 
-    python tools/ref_config2_golden.py [threads]
+    python tools/ref_config2_golden.py [threads] [config2|config1]
 
 Workload = bench.py's config 2 (180x210x180 brain-like pair, seed 2006, K=32,
 nt=10, deformation-state, sigma2=0.01, OptimizeOptions defaults, max_iter=10).
@@ -20,10 +20,13 @@ from paper_2006_06823_b200 import phantoms  # noqa: E402
 
 threads = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 dims, band, nt, sigma2 = (180, 210, 180), (32, 32, 32), 10, 0.01
-if len(sys.argv) > 2 and sys.argv[2] == "small":
-    dims, band = (64, 64, 64), (16, 16, 16)
+mode = sys.argv[2] if len(sys.argv) > 2 else "config2"
 ref.set_threads(threads)
-I0, I1 = phantoms.brain_pair(dims, seed=2006)
+if mode == "config1":  # BASELINE.json configs[0]: 64^3 sphere -> ellipsoid, K = 16
+    dims, band = (64, 64, 64), (16, 16, 16)
+    I0, I1 = phantoms.sphere_ellipsoid_pair(64)
+else:
+    I0, I1 = phantoms.brain_pair(dims, seed=2006)
 # the engine consumes fp32 images; feed the reference the identical values
 I0 = I0.astype(np.float32).astype(np.float64)
 I1 = I1.astype(np.float32).astype(np.float64)
@@ -34,7 +37,7 @@ wall = time.time() - t0
 hist = np.array([[q.iter, q.energy, q.energy_data, q.energy_reg, q.mse_rel, q.rel_grad, q.pcg_iters,
                   q.pcg_fallback, q.epsilon, q.cfl] for q in r["history"]])
 fwd, inv, jac = m.maps(r["v"])
-tag = "config2" if dims[0] == 180 else "small"
+tag = mode
 np.savez_compressed(os.path.join(ROOT, "tests", "golden", f"{tag}_ref.npz"), dims=np.array(dims),
                     band=np.array(band), nt=nt, sigma2=sigma2, history=hist, v=r["v"],
                     stop=ref.STOP_REASONS.index(r["stop"]), iterations=r["iterations"], jac=jac,
