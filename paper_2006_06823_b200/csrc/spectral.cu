@@ -262,8 +262,84 @@ void launch_band_finalize(const FinArgs& a, const DftPlan& p, const float2* G, c
   LDDMM_LAUNCH_CHECK();
 }
 
+// Batched complex GEMM for the y stages (small M x N per batch item, K up to Ny):
+// the twiddle matrix A and one whole B slab live in shared memory, so the K loop
+// runs without barriers; one batch item per CTA iteration, 2 x 2 complex outputs
+// per thread.  (The k-chunked cgemm_kernel spent most of its time in barriers and
+// global-load latency on these shapes.)
+__device__ __forceinline__ void cp_async8_f2(float2* smem, const float2* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restrict__ A, int lda,
+                                                         const float2* __restrict__ B, long long sB, int ldb,
+                                                         float2* __restrict__ C, long long sC, int ldc, int M, int N,
+                                                         int K, int batch) {
+  extern __shared__ float2 sm2[];
+  const int KP = K + 1;  // padded A row (bank spread across rows)
+  float2* As = sm2;
+  float2* Bs = sm2 + (long long)M * KP;
+  // cp.async (8-byte) copies: every element in flight at once, no register round trip
+  for (int e = threadIdx.x; e < M * K; e += blockDim.x) {
+    const int m = e / K, k = e - (e / K) * K;
+    cp_async8_f2(As + m * KP + k, A + (long long)m * lda + k);
+  }
+  const int tn = (N + 1) / 2, tiles = ((M + 1) / 2) * tn;
+  for (int b = blockIdx.x; b < batch; b += gridDim.x) {
+    __syncthreads();
+    const float2* Bb = B + b * sB;
+    for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+      const int k = e / N, n = e - (e / N) * N;
+      cp_async8_f2(Bs + e, Bb + (long long)k * ldb + n);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    float2* Cb = C + b * sC;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+      const int m0 = (t / tn) * 2, n0 = (t - (t / tn) * tn) * 2;
+      const int m1 = min(m0 + 1, M - 1), n1 = min(n0 + 1, N - 1);
+      float2 c00 = make_float2(0.f, 0.f), c01 = c00, c10 = c00, c11 = c00;
+      const float2* a0p = As + m0 * KP;
+      const float2* a1p = As + m1 * KP;
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) {
+        const float2 a0 = a0p[k], a1 = a1p[k];
+        const float2 b0 = Bs[k * N + n0], b1 = Bs[k * N + n1];
+        c00.x = fmaf(a0.x, b0.x, fmaf(-a0.y, b0.y, c00.x));
+        c00.y = fmaf(a0.x, b0.y, fmaf(a0.y, b0.x, c00.y));
+        c01.x = fmaf(a0.x, b1.x, fmaf(-a0.y, b1.y, c01.x));
+        c01.y = fmaf(a0.x, b1.y, fmaf(a0.y, b1.x, c01.y));
+        c10.x = fmaf(a1.x, b0.x, fmaf(-a1.y, b0.y, c10.x));
+        c10.y = fmaf(a1.x, b0.y, fmaf(a1.y, b0.x, c10.y));
+        c11.x = fmaf(a1.x, b1.x, fmaf(-a1.y, b1.y, c11.x));
+        c11.y = fmaf(a1.x, b1.y, fmaf(a1.y, b1.x, c11.y));
+      }
+      Cb[(long long)m0 * ldc + n0] = c00;
+      if (n0 + 1 < N) Cb[(long long)m0 * ldc + n0 + 1] = c01;
+      if (m0 + 1 < M) {
+        Cb[(long long)(m0 + 1) * ldc + n0] = c10;
+        if (n0 + 1 < N) Cb[(long long)(m0 + 1) * ldc + n0 + 1] = c11;
+      }
+    }
+  }
+}
+
 void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int ldb, float2* C, long long sC,
                   int ldc, int M, int N, int K, int batch, cudaStream_t s) {
+  const size_t smem = ((size_t)M * (K + 1) + (size_t)K * N) * sizeof(float2);
+  if (N <= 64 && smem <= 200 * 1024) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    LDDMM_CUDA(cudaGetDevice(&dev));
+    if (!attr_set[dev & 63]) {
+      LDDMM_CUDA(cudaFuncSetAttribute(cgemm_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_set[dev & 63] = true;
+    }
+    cgemm_smem_kernel<<<batch, 256, smem, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch);
+    LDDMM_LAUNCH_CHECK();
+    return;
+  }
   dim3 grid(ceil_div(N, CG_BN), ceil_div(M, CG_BM), batch);
   cgemm_kernel<<<grid, 256, 0, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K);
   LDDMM_LAUNCH_CHECK();
