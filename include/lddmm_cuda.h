@@ -51,7 +51,8 @@ typedef struct lddmm_ctx lddmm_ctx;
 
 /* Model<BandAlgebra> construction data: GridSpec (core.hpp:42-122), BandSpec
  * (spectral.hpp:22-83), Model fields variant/nt/sigma2/lop (variants.hpp:237-244),
- * SobolevOperator (spectral.hpp:518-525).  Only d = 3 and the SL integrator. */
+ * SobolevOperator (spectral.hpp:518-525).  d = 3, band representation, SL
+ * integrator; all three variants; stationary and nonstationary. */
 typedef struct {
   int d;
   int dims[3];
@@ -190,6 +191,30 @@ int lddmm_op_gather(lddmm_ctx* ctx, int impl, const float* dev_coef, int ncomp, 
 /* cubic pull-back of grid scalar fields through x - disp (warp with
  * points_from_displacement, interp.hpp:178-210, variants.hpp:49-51); disp phys units */
 int lddmm_op_warp(lddmm_ctx* ctx, const float* dev_field, int ncomp, const float* dev_disp, float* dev_out);
+
+/* ---- evaluation path (metrics.hpp:24-131, interp.hpp:178-225) ---- */
+/* Interp (interp.hpp:14) plus the nearest-neighbour label warp */
+enum { LDDMM_INTERP_LINEAR = 0, LDDMM_INTERP_CUBIC = 1, LDDMM_INTERP_NEAREST = 2 };
+/* warp_nearest(f, x - disp) (interp.hpp:213-225) on device fp32 buffers, disp phys units */
+int lddmm_op_warp_nearest(lddmm_ctx* ctx, const float* dev_field, int ncomp, const float* dev_disp, float* dev_out);
+/* map_jacobian_determinant + value_range (metrics.hpp:40-79) of a device grid displacement
+ * [3][N] (phys units); full-grid spectral derivatives in fp64; dev_det may be NULL */
+int lddmm_op_jacobian(lddmm_ctx* ctx, const float* dev_disp, float* dev_det, double minmax[2]);
+/* mean_dice (metrics.hpp:92-131) of two device label fields: inventory = distinct nonzero
+ * values of dev_target, exact integer counts on the device */
+int lddmm_op_mean_dice(lddmm_ctx* ctx, const float* dev_warped, const float* dev_target, double* out);
+
+/* Host-buffer forms (fp64, ScalarField / VectorField layouts) used by the CLI
+ * (lddmm_cli.cpp:101-235).  warp: kind LDDMM_INTERP_CUBIC (warp, interp.hpp:178-210)
+ * or LDDMM_INTERP_NEAREST; ncomp fields of N; disp [3][N] phys units. */
+int lddmm_warp(lddmm_ctx* ctx, int kind, const double* host_field, int ncomp, const double* host_disp,
+               double* host_out);
+int lddmm_jacobian(lddmm_ctx* ctx, const double* host_disp, double* host_det, double minmax[2]);
+int lddmm_mean_dice(lddmm_ctx* ctx, const double* host_warped, const double* host_target, double* out);
+/* Alg::from_spatial (= project) of a host vector field into every node of dev_v (--v0,
+ * lddmm_cli.cpp:111-117); Alg::to_spatial (= embed) of node `node` to a host vector field */
+int lddmm_vel_from_spatial(lddmm_ctx* ctx, const double* host_vec, double* dev_v);
+int lddmm_vel_to_spatial(lddmm_ctx* ctx, const double* dev_v, int node, double* host_vec);
 
 #ifdef __cplusplus
 }

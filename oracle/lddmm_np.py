@@ -857,6 +857,24 @@ def mse_rel(warped, target, source, g: Grid):  # metrics.hpp:82-89
     return 0.0 if d <= 0 else l2_inner(num, num, g) / d
 
 
+def dice(a, b, label):  # metrics.hpp:97-112 -> (dsc, both_empty)
+    ia, ib = (a == label), (b == label)
+    na, nb, nab = int(ia.sum()), int(ib.sum()), int((ia & ib).sum())
+    if na + nb == 0:
+        return 1.0, True
+    return 2.0 * nab / (na + nb), False
+
+
+def mean_dice(warped_labels, target_labels):  # metrics.hpp:114-131 (labels ascending, std::set)
+    labels = sorted(set(np.unique(target_labels[target_labels != 0]).tolist()))
+    if not labels:
+        return dice(warped_labels, target_labels, 1.0)[0]
+    s = 0.0
+    for lab in labels:
+        s += dice(warped_labels, target_labels, lab)[0]
+    return s / len(labels)
+
+
 def rescale_unit(f):  # io.hpp:166-178
     lo, hi = float(np.min(f)), float(np.max(f))
     if hi > lo:

@@ -416,6 +416,28 @@ def two_disc_case(dims, spacing, seed):
     return tuple(b for b, _ in ptrs)
 
 
+def evaluate(dims, spacing, warped=None, target=None, source=None, warped_labels=None, target_labels=None,
+             disp=None):
+    """mse_rel / mean_dice / map_jacobian_determinant + value_range (metrics.hpp:40-131)."""
+    d, di, hi = _grid_args(dims, spacing)
+    keep = []
+
+    def arg(x):
+        if x is None:
+            return None
+        b, p = _d(np.asarray(x, dtype=np.float64))
+        keep.append(b)
+        return p
+    mse, dice = C.c_double(-1.0), C.c_double(-1.0)
+    jac = np.zeros(2)
+    det = np.zeros(tuple(dims))
+    jb, jp = _d(jac)
+    db, dp = _d(det)
+    _check(lib().ref_evaluate(d, di, hi, arg(warped), arg(target), arg(source), arg(warped_labels),
+                              arg(target_labels), arg(disp), C.byref(mse), C.byref(dice), jp, dp), "evaluate")
+    return dict(mse_rel=mse.value, dice_mean=dice.value, jac=jb.copy(), det=db.copy())
+
+
 def random_band_field(dims, spacing, band, seed, amplitude, k0):
     d, di, hi = _grid_args(dims, spacing)
     out = np.zeros(d * int(np.prod(band)) * 2)

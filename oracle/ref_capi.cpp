@@ -452,6 +452,26 @@ int ref_two_disc_case(int d, const int* dims, const double* h, unsigned long lon
   });
 }
 
+// ---- metrics.hpp evaluation path: mse_rel, mean_dice, map_jacobian_determinant ------
+int ref_evaluate(int d, const int* dims, const double* h, const double* warped, const double* target,
+                 const double* source, const double* warped_labels, const double* target_labels,
+                 const double* disp, double* mse, double* dice_mean, double* jac_minmax, double* det) {
+  return guard([&] {
+    GridSpec g = make_grid(d, dims, h);
+    if (warped && target && source)
+      *mse = mse_rel(scalar_in(g, warped), scalar_in(g, target), scalar_in(g, source));
+    if (warped_labels && target_labels)
+      *dice_mean = mean_dice(scalar_in(g, warped_labels), scalar_in(g, target_labels));
+    if (disp) {
+      ScalarField j = map_jacobian_determinant(vector_in(g, disp));
+      ValueRange r = value_range(j);
+      jac_minmax[0] = r.min;
+      jac_minmax[1] = r.max;
+      if (det) scalar_out(j, det);
+    }
+  });
+}
+
 int ref_random_band_field(int d, const int* dims, const double* h, const int* band, unsigned long long seed,
                           double amplitude, double k0, double* out) {
   return guard([&] {

@@ -1,5 +1,8 @@
 // extern "C" implementation of include/lddmm_cuda.h over Engine / optimize.
+#include <algorithm>
 #include <cstring>
+#include <unordered_set>
+#include <vector>
 #include <memory>
 #include <string>
 
@@ -386,6 +389,152 @@ int lddmm_op_warp(lddmm_ctx* ctx, const float* field, int ncomp, const float* di
   return guard(ctx, [&] {
     ctx->eng->warp_grid(field, ncomp, disp, out);
     ctx->eng->sync();
+  });
+}
+
+}  // extern "C"
+
+// ---- evaluation path --------------------------------------------------------------
+
+namespace {
+
+// distinct nonzero label values in ascending order (metrics.hpp:120-126: std::set)
+std::vector<float> label_inventory(const float* host, long long n) {
+  std::unordered_set<float> seen;
+  for (long long i = 0; i < n; ++i)
+    if (host[i] != 0.0f) seen.insert(host[i]);
+  std::vector<float> v(seen.begin(), seen.end());
+  std::sort(v.begin(), v.end());
+  return v;
+}
+
+// mean_dice (metrics.hpp:97-131) from device counts; same per-label ratio and
+// ascending-label summation order as the reference
+double mean_dice_dev(Engine& e, const float* a, const float* b) {
+  const long long N = e.npts();
+  std::vector<float> hb(N);
+  LDDMM_CUDA(cudaMemcpyAsync(hb.data(), b, N * sizeof(float), cudaMemcpyDeviceToHost, e.stream()));
+  e.sync();
+  std::vector<float> labels = label_inventory(hb.data(), N);
+  const bool empty = labels.empty();
+  if (empty) labels.push_back(1.0f);  // dice(warped, target, 1.0) (metrics.hpp:128)
+  const int nl = (int)labels.size();
+  DevBuf<float> dl(nl);
+  DevBuf<unsigned long long> dc(3 * nl);
+  LDDMM_CUDA(cudaMemcpyAsync(dl.p, labels.data(), nl * sizeof(float), cudaMemcpyHostToDevice, e.stream()));
+  e.dice_counts(a, b, dl.p, nl, dc.p);
+  std::vector<unsigned long long> c(3 * nl);
+  LDDMM_CUDA(cudaMemcpyAsync(c.data(), dc.p, 3 * nl * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             e.stream()));
+  e.sync();
+  double s = 0.0;
+  for (int l = 0; l < nl; ++l) {
+    const unsigned long long na = c[3 * l], nb = c[3 * l + 1], nab = c[3 * l + 2];
+    const double dsc = na + nb == 0 ? 1.0 : 2.0 * (double)nab / (double)(na + nb);
+    if (empty) return dsc;
+    s += dsc;
+  }
+  return s / (double)nl;
+}
+
+void upload_f32(Engine& e, const double* host, long long n, float* dev) {
+  DevBuf<double> t(n);
+  LDDMM_CUDA(cudaMemcpyAsync(t.p, host, n * sizeof(double), cudaMemcpyHostToDevice, e.stream()));
+  launch_f64_to_f32(n, t.p, dev, e.stream());
+  e.sync();
+}
+
+void download_f64(Engine& e, const float* dev, long long n, double* host) {
+  DevBuf<double> t(n);
+  launch_f32_to_f64(n, dev, t.p, e.stream());
+  LDDMM_CUDA(cudaMemcpyAsync(host, t.p, n * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+  e.sync();
+}
+
+}  // namespace
+
+extern "C" {
+
+int lddmm_op_warp_nearest(lddmm_ctx* ctx, const float* field, int ncomp, const float* disp, float* out) {
+  return guard(ctx, [&] {
+    shape_require(ncomp >= 1, "warp_nearest: ncomp >= 1");
+    ctx->eng->warp_nearest(field, ncomp, disp, out);
+    ctx->eng->sync();
+  });
+}
+
+int lddmm_op_jacobian(lddmm_ctx* ctx, const float* disp, float* det, double minmax[2]) {
+  return guard(ctx, [&] { ctx->eng->jacobian_grid(disp, det, minmax); });
+}
+
+int lddmm_op_mean_dice(lddmm_ctx* ctx, const float* a, const float* b, double* out) {
+  return guard(ctx, [&] { *out = mean_dice_dev(*ctx->eng, a, b); });
+}
+
+int lddmm_warp(lddmm_ctx* ctx, int kind, const double* field, int ncomp, const double* disp, double* out) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts();
+    shape_require(kind == LDDMM_INTERP_CUBIC || kind == LDDMM_INTERP_NEAREST,
+                  "lddmm_warp: kind must be LDDMM_INTERP_CUBIC or LDDMM_INTERP_NEAREST");
+    shape_require(ncomp >= 1 && ncomp <= 6, "lddmm_warp: 1..6 components");
+    DevBuf<float> f(ncomp * N), d(3 * N), o(ncomp * N);
+    upload_f32(e, field, ncomp * N, f.p);
+    upload_f32(e, disp, 3 * N, d.p);
+    if (kind == LDDMM_INTERP_CUBIC)
+      e.warp_grid(f.p, ncomp, d.p, o.p);
+    else
+      e.warp_nearest(f.p, ncomp, d.p, o.p);
+    download_f64(e, o.p, ncomp * N, out);
+  });
+}
+
+int lddmm_jacobian(lddmm_ctx* ctx, const double* disp, double* det, double minmax[2]) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts();
+    DevBuf<float> d(3 * N);
+    upload_f32(e, disp, 3 * N, d.p);
+    DevBuf<float> o(det ? N : 1);
+    e.jacobian_grid(d.p, det ? o.p : nullptr, minmax);
+    if (det) download_f64(e, o.p, N, det);
+  });
+}
+
+int lddmm_mean_dice(lddmm_ctx* ctx, const double* a, const double* b, double* out) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts();
+    DevBuf<float> da(N), db(N);
+    upload_f32(e, a, N, da.p);
+    upload_f32(e, b, N, db.p);
+    *out = mean_dice_dev(e, da.p, db.p);
+  });
+}
+
+int lddmm_vel_from_spatial(lddmm_ctx* ctx, const double* host_vec, double* v) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts(), V = e.vec_elems();
+    DevBuf<float> g(3 * N);
+    upload_f32(e, host_vec, 3 * N, g.p);
+    e.project(g.p, 3, D2(v));
+    const int nodes = (int)(e.vel_elems() / V);
+    for (int i = 1; i < nodes; ++i)
+      LDDMM_CUDA(cudaMemcpyAsync(D2(v) + i * V, D2(v), V * sizeof(double2), cudaMemcpyDeviceToDevice, e.stream()));
+    e.sync();
+  });
+}
+
+int lddmm_vel_to_spatial(lddmm_ctx* ctx, const double* v, int node, double* host_vec) {
+  return guard(ctx, [&] {
+    Engine& e = *ctx->eng;
+    const long long N = e.npts(), V = e.vec_elems();
+    const int nodes = (int)(e.vel_elems() / V);
+    shape_require(node >= 0 && node < nodes, "lddmm_vel_to_spatial: node out of range");
+    DevBuf<float> g(3 * N);
+    e.embed(D2(v) + node * V, 3, g.p, false);
+    download_f64(e, g.p, 3 * N, host_vec);
   });
 }
 

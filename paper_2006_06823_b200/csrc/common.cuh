@@ -46,6 +46,10 @@ constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// grid-stride loop over [0, n)
+#define GRID_STRIDE(i, n) \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (n); i += (long long)gridDim.x * blockDim.x)
+
 // Grid-stride launch size: a multiple of the SM count, capped.
 inline int grid_for(long long n, int block, int per_sm = 8) {
   long long g = (n + block - 1) / block;

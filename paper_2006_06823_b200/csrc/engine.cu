@@ -285,22 +285,10 @@ void Engine::set_images_impl(const double* I0d) {
   launch_prefilter3d(c, full_.N, stream_);
   launch_f64_to_f32(N, c, I0coef_.p, stream_);
   // spectral_gradient(I0) (spectral.hpp:326-334,356-370) in fp64: per axis a real
-  // circulant derivative kernel D_a[d] = (1/n) sum_k i omega_k e^{2 pi i k d / n}
-  // (Nyquist k = n/2 excluded, omega = 2 pi k / (n h)), then the spline prefilter.
+  // circulant derivative kernel, then the spline prefilter.
+  ensure_dker();
   for (int a = 0; a < 3; ++a) {
-    const int n = full_.N[a];
-    std::vector<double> Dh(n);
-    for (int d = 0; d < n; ++d) {
-      long double acc = 0.0L;
-      for (int k = -n / 2 + 1; k < n / 2; ++k) {
-        const long double om = 2.0L * 3.14159265358979323846264338327950288L * k / (n * h_[a]);
-        const long long r = (((long long)k * d) % n + n) % n;
-        acc += -om * sinl(2.0L * 3.14159265358979323846264338327950288L * r / n);
-      }
-      Dh[d] = (double)(acc / n);
-    }
     double* g = f64b_.p;
-    LDDMM_CUDA(cudaMemcpyAsync(dker_.p + 1024 * a, Dh.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream_));
     launch_circulant_axis_f64(I0d, g, dker_.p + 1024 * a, a, full_.N, stream_);
     launch_prefilter3d(g, full_.N, stream_);
     launch_f64_to_f32(N, g, I0coef_.p + (a + 1) * N, stream_);
@@ -831,6 +819,60 @@ void Engine::series(int which, double2* out) {
   LDDMM_CUDA(cudaMemcpyAsync(out, which == 0 ? u_.p : rho_.p, (prob_.nt + 1) * V * sizeof(double2),
                              cudaMemcpyDeviceToDevice, stream_));
   sync();
+}
+
+// Circulant spectral-derivative kernels D_a[d] = (1/n) sum_k i omega_k e^{2 pi i k d / n}
+// (grid Nyquist k = n/2 excluded, omega = 2 pi k / (n h)): a full-grid
+// spectral_derivative (spectral.hpp:326-334,339-354) as an exact real convolution.
+void Engine::ensure_dker() {
+  if (dker_ready_) return;
+  for (int a = 0; a < 3; ++a) {
+    const int n = full_.N[a];
+    shape_require(n <= 1024, "spectral derivative: axis length > 1024");
+    std::vector<double> Dh(n);
+    for (int d = 0; d < n; ++d) {
+      long double acc = 0.0L;
+      for (int k = -n / 2 + 1; k < n / 2; ++k) {
+        const long double om = 2.0L * 3.14159265358979323846264338327950288L * k / (n * h_[a]);
+        const long long r = (((long long)k * d) % n + n) % n;
+        acc += -om * sinl(2.0L * 3.14159265358979323846264338327950288L * r / n);
+      }
+      Dh[d] = (double)(acc / n);
+    }
+    LDDMM_CUDA(cudaMemcpyAsync(dker_.p + 1024 * a, Dh.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    LDDMM_CUDA(cudaStreamSynchronize(stream_));
+  }
+  dker_ready_ = true;
+}
+
+void Engine::warp_nearest(const float* f, int ncomp, const float* disp_phys, float* out) {
+  launch_warp_nearest(f, ncomp, disp_phys, h_, out, full_.N, stream_);
+}
+
+// map_jacobian_determinant + value_range (metrics.hpp:40-79) of a grid displacement
+void Engine::jacobian_grid(const float* disp, float* det, double mm[2]) {
+  const long long N = npts();
+  ensure_dker();
+  if (maps_du_.n < (size_t)(9 * N)) maps_du_.alloc(9 * N);
+  for (int a = 0; a < 3; ++a) {
+    launch_f32_to_f64(N, disp + a * N, f64a_.p, stream_);
+    for (int b = 0; b < 3; ++b) {
+      launch_circulant_axis_f64(f64a_.p, f64b_.p, dker_.p + 1024 * b, b, full_.N, stream_);
+      launch_f64_to_f32(N, f64b_.p, maps_du_.p + (3 * a + b) * N, stream_);
+    }
+  }
+  if (det) launch_jacdet(N, maps_du_.p, det, stream_);
+  const int g = launch_jacdet_minmax(N, maps_du_.p, part_.p, part2_.p, stream_);
+  launch_reduce_final(part_.p, g, 1, slots_.p + 2, stream_);
+  launch_reduce_final(part2_.p, g, 1, slots_.p + 3, stream_);
+  LDDMM_CUDA(cudaMemcpyAsync(host_slots_ + 2, slots_.p + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  mm[0] = -host_slots_[2];
+  mm[1] = host_slots_[3];
+}
+
+void Engine::dice_counts(const float* a, const float* b, const float* labels, int nl, unsigned long long* counts) {
+  launch_dice_counts(npts(), a, b, labels, nl, counts, stream_);
 }
 
 // compute_maps + map_jacobian_determinant + value_range (metrics.hpp:24-79)

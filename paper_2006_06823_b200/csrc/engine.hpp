@@ -126,6 +126,14 @@ class Engine {
   void warp_grid(const float* f, int ncomp, const float* disp_phys, float* out);
   // endpoint maps and Jacobian ranges (metrics.hpp:24-65); disp outputs optional (device, [3][N] fp32)
   void maps(const double2* v, float* disp_fwd, float* disp_inv, double jac[4]);
+  // ---- evaluation path (metrics.hpp:40-131, interp.hpp:213-225) ----
+  // nearest-neighbour pull-back of grid fields (labels) through x - disp_phys
+  void warp_nearest(const float* f, int ncomp, const float* disp_phys, float* out);
+  // det(I - Du) of a grid displacement [3][N] (phys units), full-grid spectral
+  // derivatives in fp64; det optional (device fp32 [N]); mm = {min, max}
+  void jacobian_grid(const float* disp_phys, float* det, double mm[2]);
+  // Dice counts of `nl` label values: counts[3*l + {0,1,2}] = |a=l|, |b=l|, |a=l & b=l|
+  void dice_counts(const float* a, const float* b, const float* labels, int nl, unsigned long long* counts);
   void series(int which, double2* out);  // 0 u, 1 rho (nt+1 band vectors)
 
   // counters (kernel launches issued by this engine)
@@ -191,6 +199,8 @@ class Engine {
   DevBuf<float> lcoef_;       // state: spline coefficients of lambda1 / dlambda1, [N]
   DevBuf<double2> m0_;        // original: pi(I0)
   DevBuf<double> f64a_, f64b_, f64c_, dker_;  // fp64 grid scratch (image constants), derivative kernels
+  bool dker_ready_ = false;
+  void ensure_dker();  // per-axis circulant spectral-derivative kernels (spectral.hpp:326-370)
   DevBuf<float> maps_du_;     // 9 derivative fields for the Jacobian (allocated on first use)
   DevBuf<double2> opt_ws_;    // optimizer workspace: 9 velocities
 

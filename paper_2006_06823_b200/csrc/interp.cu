@@ -661,6 +661,38 @@ void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp
 }
 
 // ---------------------------------------------------------------------------
+// warp_nearest (interp.hpp:213-225): the point x - d is divided by h and rounded
+// half away from zero (std::llround), then wrapped periodically; label values are
+// copied, never mixed.
+__global__ void warp_nearest_kernel(const float* __restrict__ f, int ncomp, const float* __restrict__ disp,
+                                    double hx, double hy, double hz, float* __restrict__ out, int Nx, int Ny,
+                                    int Nz) {
+  const long long N = (long long)Nx * Ny * Nz;
+  GRID_STRIDE(p, N) {
+    const int k = (int)(p % Nz);
+    const long long q = p / Nz;
+    const int j = (int)(q % Ny), i = (int)(q / Ny);
+    const double ux = ((double)i * hx - (double)disp[p]) / hx;
+    const double uy = ((double)j * hy - (double)disp[N + p]) / hy;
+    const double uz = ((double)k * hz - (double)disp[2 * N + p]) / hz;
+    long long ix = llround(ux) % Nx, iy = llround(uy) % Ny, iz = llround(uz) % Nz;
+    ix += ix < 0 ? Nx : 0;
+    iy += iy < 0 ? Ny : 0;
+    iz += iz < 0 ? Nz : 0;
+    const long long src = (ix * Ny + iy) * Nz + iz;
+    for (int c = 0; c < ncomp; ++c) out[c * N + p] = f[c * N + src];
+  }
+}
+
+void launch_warp_nearest(const float* f, int ncomp, const float* disp_phys, const double* h, float* out,
+                         const int* N, cudaStream_t s) {
+  const long long n = (long long)N[0] * N[1] * N[2];
+  warp_nearest_kernel<<<grid_for(n, 256), 256, 0, s>>>(f, ncomp, disp_phys, h[0], h[1], h[2], out, N[0], N[1],
+                                                       N[2]);
+  LDDMM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
 // exact periodic cubic B-spline prefilter along one axis (interp.hpp:23-63),
 // one thread per line, in place (the causal pass overwrites the line with c+,
 // the anticausal pass overwrites c+ with 6 c-).

@@ -96,6 +96,10 @@ void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float
 // (points_from_displacement, variants.hpp:49-51); out[c] for ncomp coefficient fields
 void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp_phys, const double* h,
                                  float* out, const int* N, cudaStream_t s);
+// nearest-neighbour pull-back (warp_nearest, interp.hpp:213-225): out[c](x) =
+// f[c](wrap(llround((x - disp(x)) / h))), fp64 index arithmetic
+void launch_warp_nearest(const float* f, int ncomp, const float* disp_phys, const double* h, float* out,
+                         const int* N, cudaStream_t s);
 // exact periodic prefilter (interp.hpp:23-63) along every axis, fp64, in place
 void launch_prefilter3d(double* f, const int* N, cudaStream_t s);
 void launch_prefilter3d_f32(float* f, const int* N, cudaStream_t s);
@@ -149,6 +153,10 @@ void launch_jac_batch(bool transpose, int nn, long long M, const float* derivs, 
 // det(I - Du) min/max from 9 derivative fields [a][b][N] (metrics.hpp:40-65)
 int launch_jacdet_minmax(long long n, const float* du, double* part_min, double* part_max, cudaStream_t s);
 void launch_jacdet(long long n, const float* du, float* out, cudaStream_t s);
+// Dice counts (metrics.hpp:100-118) for nl label values (device array): counts[3 l + 0..2] =
+// |a == l|, |b == l|, |a == l && b == l|; counts zeroed by the launcher
+void launch_dice_counts(long long n, const float* a, const float* b, const float* labels, int nl,
+                        unsigned long long* counts, cudaStream_t s);
 // affine: out = a * x + b  (fp32 grid)
 void launch_affine_f32(long long n, const float* x, float a, float b, float* out, cudaStream_t s);
 void launch_mul_f32(long long n, const float* x, const float* y, float* out, cudaStream_t s);

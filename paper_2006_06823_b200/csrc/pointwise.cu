@@ -10,9 +10,6 @@
 
 namespace lddmm_b200 {
 
-#define GRID_STRIDE(i, n) \
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (n); i += (long long)gridDim.x * blockDim.x)
-
 __global__ void f64_to_f32_kernel(long long n, const double* __restrict__ in, float* __restrict__ out) {
   GRID_STRIDE(i, n) out[i] = (float)in[i];
 }
@@ -255,6 +252,43 @@ __global__ void jacdet_kernel(long long n, const float* __restrict__ du, float* 
 void launch_jacdet(long long n, const float* du, float* out, cudaStream_t s) {
   jacdet_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, du, out);
   LDDMM_LAUNCH_CHECK();
+}
+
+// Dice counts (metrics.hpp:100-118): per-block shared counters, one atomic per
+// counter per block.  Exact integer counts, so the host-side Dice ratio is
+// bitwise the reference's.
+constexpr int DICE_MAXL = 64;
+__global__ __launch_bounds__(256) void dice_counts_kernel(long long n, const float* __restrict__ a,
+                                                          const float* __restrict__ b,
+                                                          const float* __restrict__ labels, int nl,
+                                                          unsigned long long* counts) {
+  __shared__ unsigned int sc[3 * DICE_MAXL];
+  __shared__ float sl[DICE_MAXL];
+  for (int t = threadIdx.x; t < 3 * DICE_MAXL; t += blockDim.x) sc[t] = 0u;
+  for (int t = threadIdx.x; t < nl; t += blockDim.x) sl[t] = labels[t];
+  __syncthreads();
+  GRID_STRIDE(i, n) {
+    const float x = a[i], y = b[i];
+    for (int l = 0; l < nl; ++l) {
+      const bool ia = x == sl[l], ib = y == sl[l];
+      if (ia) atomicAdd(&sc[3 * l], 1u);
+      if (ib) atomicAdd(&sc[3 * l + 1], 1u);
+      if (ia && ib) atomicAdd(&sc[3 * l + 2], 1u);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 3 * nl; t += blockDim.x)
+    if (sc[t]) atomicAdd(counts + t, (unsigned long long)sc[t]);
+}
+
+void launch_dice_counts(long long n, const float* a, const float* b, const float* labels, int nl,
+                        unsigned long long* counts, cudaStream_t s) {
+  LDDMM_CUDA(cudaMemsetAsync(counts, 0, 3 * (size_t)nl * sizeof(unsigned long long), s));
+  for (int l0 = 0; l0 < nl; l0 += DICE_MAXL) {
+    const int m = nl - l0 < DICE_MAXL ? nl - l0 : DICE_MAXL;
+    dice_counts_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, a, b, labels + l0, m, counts + 3 * l0);
+    LDDMM_LAUNCH_CHECK();
+  }
 }
 
 __global__ void affine_kernel(long long n, const float* __restrict__ x, float a, float b, float* __restrict__ out) {

@@ -115,6 +115,14 @@ def lib():
             "lddmm_op_band": [vp, C.c_int, vp, vp, vp],
             "lddmm_op_warp": [vp, vp, C.c_int, vp, vp],
             "lddmm_op_gather": [vp, C.c_int, vp, C.c_int, vp, vp],
+            "lddmm_op_warp_nearest": [vp, vp, C.c_int, vp, vp],
+            "lddmm_op_jacobian": [vp, vp, vp, C.POINTER(C.c_double)],
+            "lddmm_op_mean_dice": [vp, vp, vp, C.POINTER(C.c_double)],
+            "lddmm_warp": [vp, C.c_int, vp, C.c_int, vp, vp],
+            "lddmm_jacobian": [vp, vp, vp, C.POINTER(C.c_double)],
+            "lddmm_mean_dice": [vp, vp, vp, C.POINTER(C.c_double)],
+            "lddmm_vel_from_spatial": [vp, vp, vp],
+            "lddmm_vel_to_spatial": [vp, vp, C.c_int, vp],
         }.items():
             getattr(L, name).argtypes = args
             getattr(L, name).restype = C.c_int
@@ -496,6 +504,71 @@ def compute_maps(model: Model, v: Velocity):
 
 
 # ---------------------------------------------------------------------------
+# evaluation path on host arrays (metrics.hpp:24-131, interp.hpp:178-225)
+
+INTERP = {"linear": 0, "cubic": 1, "nearest": 2}
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def warp(ctx: Context, field, disp, kind="cubic"):
+    """warp(f, x - disp, cubic) / warp_nearest(f, x - disp) (interp.hpp:178-225); field
+    [N...] or [C, N...], disp [3, N...] in physical units; fp32 on the device."""
+    f = _f64(field)
+    nc = 1 if f.ndim == 3 else f.shape[0]
+    out = np.zeros_like(f)
+    d = _f64(disp)
+    ctx.check(lib().lddmm_warp(ctx.h, INTERP[kind], f.ctypes.data_as(C.c_void_p), nc, d.ctypes.data_as(C.c_void_p),
+                               out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def jacobian(ctx: Context, disp, want_field=False):
+    """map_jacobian_determinant + value_range (metrics.hpp:40-79) of a grid displacement."""
+    d = _f64(disp)
+    det = np.zeros(d.shape[1:]) if want_field else None
+    mm = (C.c_double * 2)()
+    ctx.check(lib().lddmm_jacobian(ctx.h, d.ctypes.data_as(C.c_void_p),
+                                   det.ctypes.data_as(C.c_void_p) if want_field else None, mm))
+    return (mm[0], mm[1], det) if want_field else (mm[0], mm[1])
+
+
+def mean_dice(ctx: Context, warped_labels, target_labels):
+    """mean_dice (metrics.hpp:92-131), exact counts on the device."""
+    a, b = _f64(warped_labels), _f64(target_labels)
+    out = C.c_double()
+    ctx.check(lib().lddmm_mean_dice(ctx.h, a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                                    C.byref(out)))
+    return out.value
+
+
+def mse_rel(warped, target, source):
+    """|warped - target|^2 / |source - target|^2 (metrics.hpp:82-89), fp64 on the host
+    (the reference's scalar loop order)."""
+    w, t, s = (np.ravel(_f64(x)) for x in (warped, target, source))
+    num, den = w - t, s - t
+    d = float(np.dot(den, den))
+    return 0.0 if d <= 0.0 else float(np.dot(num, num)) / d
+
+
+def velocity_from_spatial(model: "Model", field) -> "Velocity":
+    """Alg::from_spatial (project) of a grid vector field into every node (--v0)."""
+    v = model.zero_velocity()
+    f = _f64(field)
+    model.ctx.check(lib().lddmm_vel_from_spatial(model.ctx.h, f.ctypes.data_as(C.c_void_p), v.ptr()))
+    return v
+
+
+def velocity_to_spatial(model: "Model", v: "Velocity", node=0):
+    """Alg::to_spatial (embed) of one velocity node -> [3, N...] grid field."""
+    out = np.zeros((3,) + tuple(model.grid.dims))
+    model.ctx.check(lib().lddmm_vel_to_spatial(model.ctx.h, v.ptr(), int(node), out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+# ---------------------------------------------------------------------------
 # primitives on device tensors (parity tests)
 
 
@@ -571,6 +644,30 @@ class Ops:
         self.ctx.check(lib().lddmm_op_gather(self.ctx.h, int(impl), C.c_void_p(coef.data_ptr()), nc,
                                              C.c_void_p(dep.data_ptr()), C.c_void_p(out.data_ptr())))
         return out
+
+    def warp_nearest(self, f, disp):
+        f = f.to(self.torch.float32).contiguous()
+        disp = disp.to(self.torch.float32).contiguous()
+        out = self.grid_out(f.shape[0])
+        self.ctx.check(lib().lddmm_op_warp_nearest(self.ctx.h, C.c_void_p(f.data_ptr()), f.shape[0],
+                                                   C.c_void_p(disp.data_ptr()), C.c_void_p(out.data_ptr())))
+        return out
+
+    def jacobian(self, disp):
+        disp = disp.to(self.torch.float32).contiguous()
+        det = self.grid_out(1)
+        mm = (C.c_double * 2)()
+        self.ctx.check(lib().lddmm_op_jacobian(self.ctx.h, C.c_void_p(disp.data_ptr()), C.c_void_p(det.data_ptr()),
+                                               mm))
+        return det[0], (mm[0], mm[1])
+
+    def mean_dice(self, a, b):
+        a = a.to(self.torch.float32).contiguous()
+        b = b.to(self.torch.float32).contiguous()
+        out = C.c_double()
+        self.ctx.check(lib().lddmm_op_mean_dice(self.ctx.h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                                C.byref(out)))
+        return out.value
 
     def warp(self, f, disp):
         f = f.to(self.torch.float32).contiguous()

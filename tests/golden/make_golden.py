@@ -133,6 +133,55 @@ def model_nonstationary():
     np.savez_compressed(os.path.join(HERE, "model_ns.npz"), **out)
 
 
+def synth():
+    """blob_pair / two_disc_case (synth.hpp:182-259) in 2-D and 3-D: fixtures for the CLI's
+    `synth` subcommand (lddmm_cli.cpp:264-296)."""
+    out = {}
+    for d in (2, 3):
+        dims, h = (16,) * d, (1.0,) * d
+        s, t = ref.blob_pair(dims, h, 3)
+        out[f"blobs{d}_source"], out[f"blobs{d}_target"] = s, t
+        s, t, sl, tl = ref.two_disc_case(dims, h, 5)
+        out[f"discs{d}_source"], out[f"discs{d}_target"] = s, t
+        out[f"discs{d}_source_labels"], out[f"discs{d}_target_labels"] = sl, tl
+    np.savez_compressed(os.path.join(HERE, "synth.npz"), **out)
+
+
+def evaluation():
+    """Evaluation path (metrics.hpp:40-131, interp.hpp:213-225): nearest-warped labels, Dice,
+    mse_rel and the Jacobian range of a displacement, on the 3-D disc case."""
+    dims, h = (16, 12, 14), (1.0, 1.0, 1.0)
+    s, t, sl, tl = ref.two_disc_case(dims, h, 7)
+    disp = ref.random_smooth_field(dims, h, 81, 1.0, 2.0)
+    x = np.stack(np.meshgrid(*[np.arange(n) * hh for n, hh in zip(dims, h)], indexing="ij"))
+    wl = ref.warp(sl, x - disp, dims, h, "nearest")[0]
+    ws = ref.warp(s, x - disp, dims, h, "cubic")[0]
+    e = ref.evaluate(dims, h, warped=ws, target=t, source=s, warped_labels=wl, target_labels=tl, disp=disp)
+    np.savez_compressed(os.path.join(HERE, "evaluation.npz"), dims=np.array(dims), spacing=np.array(h), source=s,
+                        target=t, source_labels=sl, target_labels=tl, disp=disp, warped_labels=wl,
+                        warped_source=ws, mse_rel=e["mse_rel"], dice_mean=e["dice_mean"], jac=e["jac"],
+                        det=e["det"])
+
+
+def cli_register():
+    """What `lddmm register` must reproduce on the 3-D disc case (cli_smoke.sh analog):
+    synth --kind discs --d 3 --n 32 --seed 5, then register --variant
+    deformation_state_equation --band 16 --sigma2 0.01 --max-iter 4 with labels
+    (lddmm_cli.cpp:101-232).  Inputs are the float32 payloads the CLI reads."""
+    dims, h, band, nt = (32, 32, 32), (1.0, 1.0, 1.0), (16, 16, 16), 5
+    s, t, sl, tl = (x.astype(np.float32).astype(np.float64) for x in ref.two_disc_case(dims, h, 5))
+    m = ref.RefModel(s, t, dims, h, band, "deformation_state_equation", nt, 0.01)
+    r = m.optimize(None, max_iter=4, pcg_max_iter=5)
+    hist = np.array([[q.iter, q.energy, q.energy_data, q.energy_reg, q.mse_rel, q.rel_grad, q.pcg_iters,
+                      q.pcg_fallback, q.epsilon, q.cfl] for q in r["history"]])
+    fwd, inv, jac = m.maps(r["v"])
+    x = np.stack(np.meshgrid(*[np.arange(n) * hh for n, hh in zip(dims, h)], indexing="ij"))
+    wl = ref.warp(sl, x - fwd, dims, h, "nearest")[0]
+    e = ref.evaluate(dims, h, warped_labels=wl, target_labels=tl)
+    np.savez_compressed(os.path.join(HERE, "cli_register.npz"), history=hist, stop=ref.STOP_REASONS.index(r["stop"]),
+                        iterations=r["iterations"], jac=jac, dice_mean=e["dice_mean"], v=r["v"])
+
+
 if __name__ == "__main__":
     if not ref.available():
         sys.exit("build oracle/_ref first: make -C oracle ref")
@@ -142,6 +191,9 @@ if __name__ == "__main__":
     model()
     optimize()
     model_nonstationary()
+    synth()
+    evaluation()
+    cli_register()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

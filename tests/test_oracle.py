@@ -186,3 +186,18 @@ def test_model_nonstationary_golden(variant):
     for q, row in zip(r["history"], hist):
         assert q["pcg_iters"] == int(row[2]) and q["epsilon"] == row[3]
         assert abs(q["energy"] - row[1]) <= 1e-9 * abs(row[1])
+
+
+def test_evaluation_golden():
+    """Evaluation path: warp_nearest, mean_dice, mse_rel, map_jacobian_determinant
+    (interp.hpp:213-225, metrics.hpp:40-131) against the reference's own outputs."""
+    z = load("evaluation")
+    g = O.Grid(tuple(int(x) for x in z["dims"]), tuple(float(x) for x in z["spacing"]))
+    x = O.identity_map(g)
+    wl = O.warp_nearest(z["source_labels"], x - z["disp"], g)
+    assert np.array_equal(wl, z["warped_labels"])
+    assert O.mean_dice(wl, z["target_labels"]) == float(z["dice_mean"])
+    assert abs(O.mse_rel(z["warped_source"], z["target"], z["source"], g) - float(z["mse_rel"])) < 1e-13
+    det = O.map_jacobian_determinant(z["disp"], g)
+    assert np.max(np.abs(det - z["det"])) < 1e-12
+    assert np.allclose([det.min(), det.max()], z["jac"], rtol=0, atol=1e-12)
