@@ -54,7 +54,11 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   shape_require(p.alpha > 0.0 && p.s >= 1, "sobolev: alpha > 0 and s >= 1 required");
   shape_require(p.variant >= 0 && p.variant <= 2, "unknown variant");
   LDDMM_CUDA(cudaSetDevice(device));
-  LDDMM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  // A blocking stream: it is ordered against the legacy default stream, so device
+  // buffers a caller fills or allocates there (torch tensors, cudaMemset) are
+  // complete before the engine reads them, and a caller's later default-stream
+  // work waits for the engine's writes.
+  LDDMM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamDefault));
   double wunit[3];
   cell_volume_ = 1.0;
   for (int a = 0; a < 3; ++a) {

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -29,6 +30,16 @@ struct Energies {
   double energy = 0, energy_reg = 0, energy_data = 0, cfl = 0;
 };
 
+// LDDMM_POISON=1: fill every new device buffer with NaNs, so reads of memory
+// no kernel wrote show up deterministically (debug aid; off by default).
+inline bool poison_allocations() {
+  static const int v = [] {
+    const char* e = std::getenv("LDDMM_POISON");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -38,7 +49,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) LDDMM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) {
+      LDDMM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+      if (poison_allocations()) LDDMM_CUDA(cudaMemset(p, 0xff, count * sizeof(T)));  // NaN fill (debug)
+    }
   }
   void release() {
     if (p) cudaFree(p);

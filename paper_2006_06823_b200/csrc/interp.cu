@@ -262,17 +262,21 @@ __global__ __launch_bounds__(GT_THREADS, 2) void gather_tiled_kernel(const float
 // ---------------------------------------------------------------------------
 // Register-window gather (the production path).  A CTA owns TX x TY full
 // z-rows of output nodes and stages the periodic (TX+4) x (TY+4) source rows of
-// FG components per stage in shared memory (row pitch RL >= Nz + 4, z halo 2),
-// double-buffered across component groups (cp.async commit groups) so the
-// staging of group g+1 overlaps the arithmetic of group g.  A thread evaluates
-// FOUR consecutive z nodes of one row: for every source row of the 5 x 5 (x, y)
-// neighbourhood it loads one aligned 8-float window (two LDS.128) covering the
-// 5-tap z stencils of the four nodes, so the shared-memory traffic per node and
-// component is 25 x 2 floats instead of 64-80.  Every axis uses the fixed
-// 5-tap window [-2, 2] with the zero weight first or last (|floor(d)| <= 1, the
-// SL regime): the sum is bitwise the reference's 4-tap accumulate<4>
-// (interp.hpp:145-156), same x-outer / y-inner order.  Nodes outside that
-// regime fall back to the global-memory path.
+// up to FG components in shared memory (row pitch P >= Nz + 4, a compile-time
+// constant so every row address below is an immediate offset, z halo 2).  A
+// thread evaluates FOUR consecutive z nodes of one row: for every source row of
+// the 5 x 5 (x, y) neighbourhood it loads one aligned 8-float window (two
+// LDS.128) covering the 5-tap z stencils of the four nodes.  Every axis uses
+// the fixed 5-tap window [-2, 2] with the zero weight first or last
+// (|floor(d)| <= 1, the SL regime): the sum is bitwise the reference's 4-tap
+// accumulate<4> (interp.hpp:145-156), same x-outer / y-inner order.  Nodes
+// outside that regime fall back to the global-memory path.
+//
+// The component count of a group (NC) is a template parameter, so the 25-row
+// loop is branch-free straight-line code the scheduler can interleave across
+// components.  Node pairs (0,1) and (2,3) share FFMA2 instructions where their
+// taps form an aligned register pair (even taps); odd taps use scalar FFMA
+// (a packed operand there would cost two MOVs).
 constexpr int GW_H = 2;
 
 __device__ __forceinline__ void w5(float d, float f, float* w) {
@@ -298,6 +302,7 @@ __device__ __forceinline__ void gw_stage(float* dst_base, const float* __restric
   constexpr int SX = TX + 2 * GW_H, SY = TY + 2 * GW_H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cvol = SX * SY * RL;
+  const int zlen = ((Nz + 3) & ~3) + 2 * GW_H;
   for (int row = warp; row < nc * SX * SY; row += NTH / 32) {
     const int c = row / (SX * SY);
     const int rr = row - c * (SX * SY);
@@ -307,7 +312,7 @@ __device__ __forceinline__ void gw_stage(float* dst_base, const float* __restric
     float* dst = dst_base + c * cvol + rr * RL;
     // 8-byte copies: Nz is even, so every pair (z, z+1), z = zz - 2 even, is contiguous
     // in global memory even across the periodic wrap
-    for (int zz = 2 * lane; zz < RL; zz += 64) {
+    for (int zz = 2 * lane; zz < zlen; zz += 64) {
       int gz = zz - GW_H;
       gz += gz < 0 ? Nz : 0;
       gz -= gz >= Nz ? Nz : 0;
@@ -316,13 +321,12 @@ __device__ __forceinline__ void gw_stage(float* dst_base, const float* __restric
   }
 }
 
-template <int FG, int TX, int TY, int NTH>
+template <int NC, int TX, int TY, int NTH, int P>
 __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __restrict__ coef,
                                            const float* __restrict__ disp, float* __restrict__ out, long long N,
-                                           int c0, int nc, int x0, int y0, int Nx, int Ny, int Nz, int RL,
-                                           float3 sc) {
+                                           int c0, int x0, int y0, int Nx, int Ny, int Nz, float3 sc) {
   constexpr int SY = TY + 2 * GW_H, SX = TX + 2 * GW_H;
-  const int cvol = SX * SY * RL;
+  constexpr int cvol = SX * SY * P;
   const int G = (Nz + 3) >> 2;
   const int items = TX * TY * G;
   const bool vec = (Nz & 3) == 0;
@@ -368,9 +372,9 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
     }
     if (!ok) {
       for (int m = 0; m < npt; ++m) {
-        float v[FG];
-        gather_point_global<FG>(coef + c0 * N, disp, i, j, z + m, Nx, Ny, Nz, nc, v, sc);
-        for (int c = 0; c < nc; ++c) out[(c0 + c) * N + p0 + m] = v[c];
+        float v[NC];
+        gather_point_global<NC>(coef + c0 * N, disp, i, j, z + m, Nx, Ny, Nz, NC, v, sc);
+        for (int c = 0; c < NC; ++c) out[(c0 + c) * N + p0 + m] = v[c];
       }
       continue;
     }
@@ -393,40 +397,44 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
 #pragma unroll
       for (int k = 0; k < 5; ++k) wz[hp][k] = make_float2(t0[k], t1[k]);
     }
-    float2 acc[FG][2];
+    float2 acc[NC][2];
 #pragma unroll
-    for (int c = 0; c < FG; ++c) acc[c][0] = acc[c][1] = make_float2(0.f, 0.f);
-    const float* base = sbuf + (rx * SY + ry) * RL + z;
+    for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = make_float2(0.f, 0.f);
+    const float* base = sbuf + (rx * SY + ry) * P + z;
 #pragma unroll
     for (int a = 0; a < 5; ++a) {
 #pragma unroll
       for (int b = 0; b < 5; ++b) {
-        const float* rowp = base + (a * SY + b) * RL;
+        const float* rowp = base + (a * SY + b) * P;
         const float2 w01a = __fmul2_rn(wx[0][a], wy[0][b]);
         const float2 w01b = __fmul2_rn(wx[1][a], wy[1][b]);
 #pragma unroll
-        for (int c = 0; c < FG; ++c) {
-          if (c < nc) {
-            const float4 A = *reinterpret_cast<const float4*>(rowp + c * cvol);
-            const float4 B = *reinterpret_cast<const float4*>(rowp + c * cvol + 4);
-            const float win[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
-            // nodes (0,1): taps win[k], win[k+1]; nodes (2,3): win[k+2], win[k+3]
-            float2 pa = __fmul2_rn(wz[0][0], make_float2(win[0], win[1]));
-            float2 pb = __fmul2_rn(wz[1][0], make_float2(win[2], win[3]));
+        for (int c = 0; c < NC; ++c) {
+          const float4 A = *reinterpret_cast<const float4*>(rowp + c * cvol);
+          const float4 B = *reinterpret_cast<const float4*>(rowp + c * cvol + 4);
+          const float win[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+          // nodes (0,1): taps win[k], win[k+1]; nodes (2,3): win[k+2], win[k+3]
+          float2 pa = __fmul2_rn(wz[0][0], make_float2(win[0], win[1]));
+          float2 pb = __fmul2_rn(wz[1][0], make_float2(win[2], win[3]));
 #pragma unroll
-            for (int k = 1; k < 5; ++k) {
+          for (int k = 1; k < 5; ++k) {
+            if (k & 1) {
+              pa.x = fmaf(wz[0][k].x, win[k], pa.x);
+              pa.y = fmaf(wz[0][k].y, win[k + 1], pa.y);
+              pb.x = fmaf(wz[1][k].x, win[k + 2], pb.x);
+              pb.y = fmaf(wz[1][k].y, win[k + 3], pb.y);
+            } else {
               pa = __ffma2_rn(wz[0][k], make_float2(win[k], win[k + 1]), pa);
               pb = __ffma2_rn(wz[1][k], make_float2(win[k + 2], win[k + 3]), pb);
             }
-            acc[c][0] = __ffma2_rn(w01a, pa, acc[c][0]);
-            acc[c][1] = __ffma2_rn(w01b, pb, acc[c][1]);
           }
+          acc[c][0] = __ffma2_rn(w01a, pa, acc[c][0]);
+          acc[c][1] = __ffma2_rn(w01b, pb, acc[c][1]);
         }
       }
     }
 #pragma unroll
-    for (int c = 0; c < FG; ++c) {
-      if (c >= nc) break;
+    for (int c = 0; c < NC; ++c) {
       float* o = out + (c0 + c) * N + p0;
       if (vec) {
         *reinterpret_cast<float4*>(o) = make_float4(acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y);
@@ -438,78 +446,62 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
   }
 }
 
-// NBUF = 1: stage FG components, compute, repeat.  NBUF = 2: double-buffered.
-template <int FG, int TX, int TY, int NTH, int MINB, int NBUF>
-__global__ __launch_bounds__(NTH, MINB) void gather_win_kernel(const float* __restrict__ coef, int F,
-                                                               const float* __restrict__ disp,
-                                                               float* __restrict__ out, int Nx, int Ny, int Nz,
-                                                               int RL, float3 sc) {
+// Components in groups of FG (single-buffered: stage, compute, repeat); the tail
+// group dispatches to the matching NC instantiation outside the row loop.
+template <int FG, int TX, int TY, int NTH, int P>
+__global__ __launch_bounds__(NTH, 1) void gather_win_kernel(const float* __restrict__ coef, int F,
+                                                            const float* __restrict__ disp, float* __restrict__ out,
+                                                            int Nx, int Ny, int Nz, float3 sc) {
   extern __shared__ __align__(16) float smw[];
-  constexpr int SX = TX + 2 * GW_H, SY = TY + 2 * GW_H;
   const long long N = (long long)Nx * Ny * Nz;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int bufvol = FG * SX * SY * RL;
-  const int ngroups = (F + FG - 1) / FG;
-  if (NBUF == 1) {
-    for (int gi = 0; gi < ngroups; ++gi) {
-      const int c0 = gi * FG, nc = min(FG, F - c0);
-      __syncthreads();
-      gw_stage<TX, TY, NTH>(smw, coef, N, c0, nc, x0, y0, Nx, Ny, Nz, RL);
-      cp_async_commit();
-      cp_async_wait_group<0>();
-      __syncthreads();
-      gw_compute<FG, TX, TY, NTH>(smw, coef, disp, out, N, c0, nc, x0, y0, Nx, Ny, Nz, RL, sc);
-    }
-  } else {
-    gw_stage<TX, TY, NTH>(smw, coef, N, 0, min(FG, F), x0, y0, Nx, Ny, Nz, RL);
+  for (int c0 = 0; c0 < F; c0 += FG) {
+    const int nc = min(FG, F - c0);
+    __syncthreads();
+    gw_stage<TX, TY, NTH>(smw, coef, N, c0, nc, x0, y0, Nx, Ny, Nz, P);
     cp_async_commit();
-    for (int gi = 0; gi < ngroups; ++gi) {
-      const int c0 = gi * FG, nc = min(FG, F - c0);
-      if (gi + 1 < ngroups) {
-        const int c1 = c0 + FG;
-        gw_stage<TX, TY, NTH>(smw + ((gi + 1) & 1) * bufvol, coef, N, c1, min(FG, F - c1), x0, y0, Nx, Ny, Nz,
-                              RL);
-        cp_async_commit();
-        cp_async_wait_group<1>();
-      } else {
-        cp_async_wait_group<0>();
-      }
-      __syncthreads();
-      gw_compute<FG, TX, TY, NTH>(smw + (gi & 1) * bufvol, coef, disp, out, N, c0, nc, x0, y0, Nx, Ny, Nz, RL,
-                                  sc);
-      __syncthreads();
-    }
+    cp_async_wait_group<0>();
+    __syncthreads();
+    if (FG >= 3 && nc == 3)
+      gw_compute<3, TX, TY, NTH, P>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
+    else if (FG >= 2 && nc == 2)
+      gw_compute<2, TX, TY, NTH, P>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
+    else
+      gw_compute<1, TX, TY, NTH, P>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
   }
 }
 
-static int gw_row_len(int Nz) { return (((Nz + 3) >> 2) << 2) + 4; }
+constexpr int GW_TX = 8, GW_TY = 4, GW_NTH = 512;
+constexpr size_t GW_SMEM_MAX = 227 * 1024;
 
-template <int FG, int TX, int TY, int NTH, int MINB, int NBUF>
-static void launch_gw(const float* coef, int ncomp, const float* disp, float* out, const int* N, int RL,
-                      float3 sc, cudaStream_t s) {
-  auto kern = gather_win_kernel<FG, TX, TY, NTH, MINB, NBUF>;
-  const size_t smem = (size_t)NBUF * FG * (TX + 4) * (TY + 4) * RL * sizeof(float);
-  static bool attr_set[64] = {false};
+template <int P>
+static bool launch_gw_pitch(const float* coef, int ncomp, const float* disp, float* out, const int* N, float3 sc,
+                            cudaStream_t s) {
+  if (((N[2] + 3) & ~3) + 2 * GW_H > P) return false;
+  const size_t per_comp = (size_t)(GW_TX + 4) * (GW_TY + 4) * P * sizeof(float);
+  const int fg = (int)std::min<size_t>(3, GW_SMEM_MAX / per_comp);
+  if (fg < 1) return false;
+  static bool attr_set[64][3] = {};
   int dev = 0;
   LDDMM_CUDA(cudaGetDevice(&dev));
-  if (!attr_set[dev & 63]) {
-    LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set[dev & 63] = true;
-  }
-  dim3 grid(ceil_div(N[0], TX), ceil_div(N[1], TY), 1);
-  kern<<<grid, NTH, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], RL, sc);
+  dim3 grid(ceil_div(N[0], GW_TX), ceil_div(N[1], GW_TY), 1);
+  const int FG = std::min(fg, ncomp);
+  const size_t smem = (size_t)FG * per_comp;
+  auto go = [&](auto kern, int k) {
+    if (!attr_set[dev & 63][k]) {
+      LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GW_SMEM_MAX));
+      attr_set[dev & 63][k] = true;
+    }
+    kern<<<grid, GW_NTH, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], sc);
+  };
+  if (FG == 3)
+    go(gather_win_kernel<3, GW_TX, GW_TY, GW_NTH, P>, 2);
+  else if (FG == 2)
+    go(gather_win_kernel<2, GW_TX, GW_TY, GW_NTH, P>, 1);
+  else
+    go(gather_win_kernel<1, GW_TX, GW_TY, GW_NTH, P>, 0);
   LDDMM_LAUNCH_CHECK();
-}
-
-// Gather variant (env LDDMM_GATHER, default 1): 1 = single-buffered FG=3 8x4 tiles
-// (1 CTA/SM); 2 = double-buffered FG=1 4x4 tiles (2 CTAs/SM).
-static int gather_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("LDDMM_GATHER");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
+  return true;
 }
 
 void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float* out, const int* N,
@@ -517,27 +509,19 @@ void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float*
   launch_gather_scaled(coef, ncomp, disp, 1.f, 1.f, 1.f, out, N, s);
 }
 
+// Row pitch: the smallest compiled pitch >= Nz + 4 (multiple of 4); z rows
+// longer than 516 go to the tiled kernel (unit scale only).
 void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
                           const int* N, cudaStream_t s) {
   const float3 sc = make_float3(sx, sy, sz);
-  const int RL = gw_row_len(N[2]);
-  const size_t smem_max = 227 * 1024;
-  const int var = gather_variant();
-  if (var == 2 && 2 * 8 * 8 * (size_t)RL * 4 <= smem_max / 2) {
-    launch_gw<1, 4, 4, 256, 2, 2>(coef, ncomp, disp, out, N, RL, sc, s);
-    return;
-  }
-  const size_t per_comp = (size_t)12 * 8 * RL * sizeof(float);
-  int FG = (int)std::min<size_t>(3, smem_max / per_comp);
-  if (FG > ncomp) FG = ncomp;
-  if (FG == 3)
-    launch_gw<3, 8, 4, 512, 1, 1>(coef, ncomp, disp, out, N, RL, sc, s);
-  else if (FG == 2)
-    launch_gw<2, 8, 4, 512, 1, 1>(coef, ncomp, disp, out, N, RL, sc, s);
-  else if (FG == 1)
-    launch_gw<1, 8, 4, 512, 1, 1>(coef, ncomp, disp, out, N, RL, sc, s);
-  else
-    launch_gather_cubic_tiled(coef, ncomp, disp, out, N, s);  // (unit scale only: huge grids)
+  if (launch_gw_pitch<64>(coef, ncomp, disp, out, N, sc, s)) return;
+  if (launch_gw_pitch<128>(coef, ncomp, disp, out, N, sc, s)) return;
+  if (launch_gw_pitch<192>(coef, ncomp, disp, out, N, sc, s)) return;
+  if (launch_gw_pitch<264>(coef, ncomp, disp, out, N, sc, s)) return;
+  if (launch_gw_pitch<392>(coef, ncomp, disp, out, N, sc, s)) return;
+  if (launch_gw_pitch<520>(coef, ncomp, disp, out, N, sc, s)) return;
+  shape_require(sx == 1.f && sy == 1.f && sz == 1.f, "gather: z rows longer than 516 need unit scale");
+  launch_gather_cubic_tiled(coef, ncomp, disp, out, N, s);
 }
 
 void launch_gather_cubic_tiled(const float* coef, int ncomp, const float* disp, float* out, const int* N,

@@ -128,12 +128,19 @@ __global__ void band_finalize_kernel(FinArgs a, int Kx, int Ky, int Kz, const fl
 
 constexpr int CG_BM = 32, CG_BN = 32, CG_BK = 16;
 
+__device__ __forceinline__ void cp_async8_f2(float2* smem, const float2* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// k-chunks staged with 8-byte cp.async and double-buffered: the next chunk
+// streams in while the current one is multiplied.
 __global__ __launch_bounds__(256) void cgemm_kernel(const float2* __restrict__ A, int lda,
                                                     const float2* __restrict__ B, long long sB, int ldb,
                                                     float2* __restrict__ C, long long sC, int ldc, int M,
                                                     int N, int K) {
-  __shared__ float2 As[CG_BK][CG_BM + 1];
-  __shared__ float2 Bs[CG_BK][CG_BN + 1];
+  __shared__ float2 As[2][CG_BK][CG_BM + 1];
+  __shared__ float2 Bs[2][CG_BK][CG_BN + 1];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int m0 = blockIdx.y * CG_BM, n0 = blockIdx.x * CG_BN;
@@ -144,22 +151,39 @@ __global__ __launch_bounds__(256) void cgemm_kernel(const float2* __restrict__ A
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
-  for (int k0 = 0; k0 < K; k0 += CG_BK) {
+  auto stage = [&](int buf, int k0) {
     for (int e = tid; e < CG_BM * CG_BK; e += 256) {
       const int mm = e / CG_BK, kk = e % CG_BK;
       const int gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < M && gk < K) ? A[(long long)gm * lda + gk] : make_float2(0.f, 0.f);
+      if (gm < M && gk < K)
+        cp_async8_f2(&As[buf][kk][mm], A + (long long)gm * lda + gk);
+      else
+        As[buf][kk][mm] = make_float2(0.f, 0.f);
     }
     for (int e = tid; e < CG_BK * CG_BN; e += 256) {
       const int kk = e / CG_BN, nn = e % CG_BN;
       const int gk = k0 + kk, gn = n0 + nn;
-      Bs[kk][nn] = (gk < K && gn < N) ? B[(long long)gk * ldb + gn] : make_float2(0.f, 0.f);
+      if (gk < K && gn < N)
+        cp_async8_f2(&Bs[buf][kk][nn], B + (long long)gk * ldb + gn);
+      else
+        Bs[buf][kk][nn] = make_float2(0.f, 0.f);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  stage(0, 0);
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += CG_BK, buf ^= 1) {
+    if (k0 + CG_BK < K) {
+      stage(buf ^ 1, k0 + CG_BK);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < CG_BK; ++kk) {
-      const float2 a0 = As[kk][ty], a1 = As[kk][ty + 16];
-      const float2 b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
+      const float2 a0 = As[buf][kk][ty], a1 = As[buf][kk][ty + 16];
+      const float2 b0 = Bs[buf][kk][tx], b1 = Bs[buf][kk][tx + 16];
       acc[0][0].x = fmaf(a0.x, b0.x, fmaf(-a0.y, b0.y, acc[0][0].x));
       acc[0][0].y = fmaf(a0.x, b0.y, fmaf(a0.y, b0.x, acc[0][0].y));
       acc[0][1].x = fmaf(a0.x, b1.x, fmaf(-a0.y, b1.y, acc[0][1].x));
@@ -267,10 +291,6 @@ void launch_band_finalize(const FinArgs& a, const DftPlan& p, const float2* G, c
 // runs without barriers; one batch item per CTA iteration, 2 x 2 complex outputs
 // per thread.  (The k-chunked cgemm_kernel spent most of its time in barriers and
 // global-load latency on these shapes.)
-__device__ __forceinline__ void cp_async8_f2(float2* smem, const float2* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
 
 __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restrict__ A, int lda,
                                                          const float2* __restrict__ B, long long sB, int ldb,
