@@ -151,6 +151,19 @@ def run_reference(args, rank, world):
     print(json.dumps(out))
 
 
+def ncu_traffic():
+    """DRAM bytes of one captured gather launch (profiles/r1_ncu_traffic.json, from
+    `ncu --set full`), next to that launch's algorithmic bytes N (12 + 8 F)."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return {"traffic": t["dram_bytes"], "traffic_launch_algorithmic_bytes": t["algorithmic_bytes"],
+                "traffic_source": "profiles/r1_ncu_traffic.json (" + t["kernel"] + ", one launch)"}
+    except (OSError, KeyError, ValueError):
+        return {"traffic": None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -235,12 +248,20 @@ def main():
     e2e = None
     if not args.no_e2e:
         ectx = L.Context(band, "deformation_state_equation", NT, SIGMA2, device=local)
+        # inputs and the result velocity in pinned host memory (the reference's fp64
+        # ScalarField / BandVectorField layouts); W untimed warm-up calls first
+        h0 = torch.from_numpy(I0.astype(np.float64)).pin_memory().numpy()
+        h1 = torch.from_numpy(I1.astype(np.float64)).pin_memory().numpy()
+        v_host = torch.zeros(ectx.vel_shape + (2,), dtype=torch.float64).pin_memory().numpy().view(np.complex128)
+        v_host = v_host.reshape(ectx.vel_shape)
+        for _ in range(max(1, args.warmup)):
+            L.register_host(ectx, h0, h1, opt, v_out=v_host)
         e_ms = []
         for k in range(max(1, args.steps)):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            v_host, r2 = L.register_host(ectx, I0, I1, opt)
+            v_host, r2 = L.register_host(ectx, h0, h1, opt, v_out=v_host)
             e_ms.append((time.perf_counter() - t0) * 1000.0)
         e2e_ms = float(np.sum(e_ms))
         if dist is not None:
@@ -250,7 +271,7 @@ def main():
             e2e_ms = max(float(x.item()) for x in allt)
         e2e = {"value": e2e_ms / 1000.0 / (world * len(e_ms)), "unit": "s/registration",
                "h2d_bytes_per_step": int(2 * I0.size * 8), "d2h_bytes_per_step": int(v_host.nbytes),
-               "path": "lddmm_register (C ABI) from host fp64 images to host fp64 velocity"}
+               "path": "lddmm_register (C ABI): pinned host fp64 images in, pinned host fp64 velocity out"}
         del ectx
 
     cpu = None
@@ -268,9 +289,9 @@ def main():
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": False,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32 grid / f64 band", "data": "synthetic",
                "config": workload(),
-               "roofline": {"kernel": "gather_cubic_kernel (SL cubic gather)", "bound": "hbm",
+               "roofline": {"kernel": "gather_win_kernel (SL cubic gather)", "bound": "hbm",
                             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                            "frac": achieved / hbm, "traffic": None,
+                            "frac": achieved / hbm, **ncu_traffic(),
                             "algorithmic_bytes_per_launch": g_bytes / g_n if g_n else 0,
                             "launches_timed": g_n, "gather_share_of_step": g_ms / total_ms if total_ms else 0},
                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),

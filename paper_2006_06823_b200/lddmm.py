@@ -473,12 +473,16 @@ def optimize(model: Model, v0: Velocity = None, opt: OptimizeOptions = None) -> 
                           res.final_energy, res.rel_grad, res.hessvecs, res.trials, res.forwards)
 
 
-def register_host(ctx: Context, I0, I1, opt: OptimizeOptions = None):
-    """End-to-end registration from host buffers (lddmm_cli.cpp:101-125): returns (v, result)."""
+def register_host(ctx: Context, I0, I1, opt: OptimizeOptions = None, v_out=None):
+    """End-to-end registration from host buffers (lddmm_cli.cpp:101-125): returns (v, result).
+    Host arrays may live in pinned memory (e.g. numpy views of pinned torch tensors);
+    v_out, when given, is a complex128 array of ctx.vel_shape that receives the velocity."""
     opt = opt or OptimizeOptions()
     I0 = np.ascontiguousarray(I0, dtype=np.float64)
     I1 = np.ascontiguousarray(I1, dtype=np.float64)
-    v = np.zeros(ctx.vel_shape, dtype=np.complex128)
+    v = v_out if v_out is not None else np.zeros(ctx.vel_shape, dtype=np.complex128)
+    if v.shape != tuple(ctx.vel_shape) or v.dtype != np.complex128 or not v.flags.c_contiguous:
+        raise ShapeError("register_host: v_out must be C-contiguous complex128 of ctx.vel_shape")
     cap = opt.max_iter + 2
     recs = (_Record * cap)()
     res = _Result()
