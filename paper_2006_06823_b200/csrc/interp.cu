@@ -125,6 +125,10 @@ __device__ __forceinline__ void cp_async8(float* smem, const float* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16_cg(float* smem, const float* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // one cubic weight (same expressions as cubic_w)
@@ -296,13 +300,18 @@ __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
 }
 
-template <int TX, int TY, int NTH>
+// Staged row layout.  SHIFT = false (any even Nz): smem index i holds z = i - 2,
+// 8-byte cp.async.  SHIFT = true (Nz % 4 == 0): index i holds z = i - 4 and the
+// node groups are shifted by -2 (group g = nodes 4g-2 .. 4g+1, group 0 wrapping
+// to Nz-2, Nz-1, 0, 1), so both the staging copies (16-byte cp.async.cg) and the
+// per-group windows (indices 4g .. 4g+7) are 16-byte aligned.
+template <int TX, int TY, int NTH, bool SHIFT>
 __device__ __forceinline__ void gw_stage(float* dst_base, const float* __restrict__ coef, long long N, int c0, int nc,
                                          int x0, int y0, int Nx, int Ny, int Nz, int RL) {
   constexpr int SX = TX + 2 * GW_H, SY = TY + 2 * GW_H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cvol = SX * SY * RL;
-  const int zlen = ((Nz + 3) & ~3) + 2 * GW_H;
+  const int zlen = SHIFT ? Nz + 8 : ((Nz + 3) & ~3) + 2 * GW_H;
   for (int row = warp; row < nc * SX * SY; row += NTH / 32) {
     const int c = row / (SX * SY);
     const int rr = row - c * (SX * SY);
@@ -310,18 +319,29 @@ __device__ __forceinline__ void gw_stage(float* dst_base, const float* __restric
     const float* src =
         coef + (c0 + c) * N + ((long long)wrapi(x0 - GW_H + ix, Nx) * Ny + wrapi(y0 - GW_H + jy, Ny)) * Nz;
     float* dst = dst_base + c * cvol + rr * RL;
-    // 8-byte copies: Nz is even, so every pair (z, z+1), z = zz - 2 even, is contiguous
-    // in global memory even across the periodic wrap
-    for (int zz = 2 * lane; zz < zlen; zz += 64) {
-      int gz = zz - GW_H;
-      gz += gz < 0 ? Nz : 0;
-      gz -= gz >= Nz ? Nz : 0;
-      cp_async8(dst + zz, src + gz);
+    if (SHIFT) {
+      // 16-byte copies: z = zz - 4 is a multiple of 4, the periodic wrap falls on
+      // 4-float boundaries
+      for (int zz = 4 * lane; zz < zlen; zz += 128) {
+        int gz = zz - 4;
+        gz += gz < 0 ? Nz : 0;
+        gz -= gz >= Nz ? Nz : 0;
+        cp_async16_cg(dst + zz, src + gz);
+      }
+    } else {
+      // 8-byte copies: Nz is even, so every pair (z, z+1), z = zz - 2 even, is
+      // contiguous in global memory even across the periodic wrap
+      for (int zz = 2 * lane; zz < zlen; zz += 64) {
+        int gz = zz - GW_H;
+        gz += gz < 0 ? Nz : 0;
+        gz -= gz >= Nz ? Nz : 0;
+        cp_async8(dst + zz, src + gz);
+      }
     }
   }
 }
 
-template <int NC, int TX, int TY, int NTH, int P>
+template <int NC, int TX, int TY, int NTH, int P, bool SHIFT>
 __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __restrict__ coef,
                                            const float* __restrict__ disp, float* __restrict__ out, long long N,
                                            int c0, int x0, int y0, int Nx, int Ny, int Nz, float3 sc) {
@@ -335,11 +355,30 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
     const int rx = r / TY, ry = r - (r / TY) * TY;
     const int i = x0 + rx, j = y0 + ry;
     if (i >= Nx || j >= Ny) continue;
-    const int z = g << 2;
-    const int npt = min(4, Nz - z);
-    const long long p0 = ((long long)i * Ny + j) * Nz + z;
+    const long long rowp0 = ((long long)i * Ny + j) * Nz;
+    // z of nodes (0,1) and (2,3) of the group
+    const int zA = SHIFT ? (g == 0 ? Nz - 2 : 4 * g - 2) : 4 * g;
+    const int zB = SHIFT ? 4 * g : 4 * g + 2;
+    const int npt = SHIFT ? 4 : min(4, Nz - 4 * g);
     float dx[4], dy[4], dz[4];
-    if (vec) {
+    if (SHIFT) {
+      const float2 ax = *reinterpret_cast<const float2*>(disp + rowp0 + zA);
+      const float2 bx = *reinterpret_cast<const float2*>(disp + rowp0 + zB);
+      const float2 ay = *reinterpret_cast<const float2*>(disp + N + rowp0 + zA);
+      const float2 by = *reinterpret_cast<const float2*>(disp + N + rowp0 + zB);
+      const float2 az = *reinterpret_cast<const float2*>(disp + 2 * N + rowp0 + zA);
+      const float2 bz = *reinterpret_cast<const float2*>(disp + 2 * N + rowp0 + zB);
+      dx[0] = ax.x; dx[1] = ax.y; dx[2] = bx.x; dx[3] = bx.y;
+      dy[0] = ay.x; dy[1] = ay.y; dy[2] = by.x; dy[3] = by.y;
+      dz[0] = az.x; dz[1] = az.y; dz[2] = bz.x; dz[3] = bz.y;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        dx[m] *= sc.x;
+        dy[m] *= sc.y;
+        dz[m] *= sc.z;
+      }
+    } else if (vec) {
+      const long long p0 = rowp0 + 4 * g;
       const float4 a = *reinterpret_cast<const float4*>(disp + p0);
       const float4 b = *reinterpret_cast<const float4*>(disp + N + p0);
       const float4 cc = *reinterpret_cast<const float4*>(disp + 2 * N + p0);
@@ -353,6 +392,7 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
         dz[m] *= sc.z;
       }
     } else {
+      const long long p0 = rowp0 + 4 * g;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const bool in = m < npt;
@@ -372,9 +412,10 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
     }
     if (!ok) {
       for (int m = 0; m < npt; ++m) {
+        const int zm = (m < 2 ? zA : zB) + (m & 1);
         float v[NC];
-        gather_point_global<NC>(coef + c0 * N, disp, i, j, z + m, Nx, Ny, Nz, NC, v, sc);
-        for (int c = 0; c < NC; ++c) out[(c0 + c) * N + p0 + m] = v[c];
+        gather_point_global<NC>(coef + c0 * N, disp, i, j, zm, Nx, Ny, Nz, NC, v, sc);
+        for (int c = 0; c < NC; ++c) out[(c0 + c) * N + rowp0 + zm] = v[c];
       }
       continue;
     }
@@ -400,7 +441,7 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
     float2 acc[NC][2];
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = make_float2(0.f, 0.f);
-    const float* base = sbuf + (rx * SY + ry) * P + z;
+    const float* base = sbuf + (rx * SY + ry) * P + 4 * g;
 #pragma unroll
     for (int a = 0; a < 5; ++a) {
 #pragma unroll
@@ -435,12 +476,15 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      float* o = out + (c0 + c) * N + p0;
-      if (vec) {
-        *reinterpret_cast<float4*>(o) = make_float4(acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y);
+      float* o = out + (c0 + c) * N + rowp0;
+      if (SHIFT) {
+        *reinterpret_cast<float2*>(o + zA) = acc[c][0];
+        *reinterpret_cast<float2*>(o + zB) = acc[c][1];
+      } else if (vec) {
+        *reinterpret_cast<float4*>(o + 4 * g) = make_float4(acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y);
       } else {
         const float v4[4] = {acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y};
-        for (int m = 0; m < npt; ++m) o[m] = v4[m];
+        for (int m = 0; m < npt; ++m) o[4 * g + m] = v4[m];
       }
     }
   }
@@ -448,7 +492,7 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
 
 // Components in groups of FG (single-buffered: stage, compute, repeat); the tail
 // group dispatches to the matching NC instantiation outside the row loop.
-template <int FG, int TX, int TY, int NTH, int P>
+template <int FG, int TX, int TY, int NTH, int P, bool SHIFT>
 __global__ __launch_bounds__(NTH, 1) void gather_win_kernel(const float* __restrict__ coef, int F,
                                                             const float* __restrict__ disp, float* __restrict__ out,
                                                             int Nx, int Ny, int Nz, float3 sc) {
@@ -458,26 +502,27 @@ __global__ __launch_bounds__(NTH, 1) void gather_win_kernel(const float* __restr
   for (int c0 = 0; c0 < F; c0 += FG) {
     const int nc = min(FG, F - c0);
     __syncthreads();
-    gw_stage<TX, TY, NTH>(smw, coef, N, c0, nc, x0, y0, Nx, Ny, Nz, P);
+    gw_stage<TX, TY, NTH, SHIFT>(smw, coef, N, c0, nc, x0, y0, Nx, Ny, Nz, P);
     cp_async_commit();
     cp_async_wait_group<0>();
     __syncthreads();
     if (FG >= 3 && nc == 3)
-      gw_compute<3, TX, TY, NTH, P>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
+      gw_compute<3, TX, TY, NTH, P, SHIFT>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
     else if (FG >= 2 && nc == 2)
-      gw_compute<2, TX, TY, NTH, P>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
+      gw_compute<2, TX, TY, NTH, P, SHIFT>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
     else
-      gw_compute<1, TX, TY, NTH, P>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
+      gw_compute<1, TX, TY, NTH, P, SHIFT>(smw, coef, disp, out, N, c0, x0, y0, Nx, Ny, Nz, sc);
   }
 }
 
 constexpr int GW_TX = 8, GW_TY = 4, GW_NTH = 512;
 constexpr size_t GW_SMEM_MAX = 227 * 1024;
 
-template <int P>
+template <int P, bool SHIFT>
 static bool launch_gw_pitch(const float* coef, int ncomp, const float* disp, float* out, const int* N, float3 sc,
                             cudaStream_t s) {
-  if (((N[2] + 3) & ~3) + 2 * GW_H > P) return false;
+  const int need = SHIFT ? N[2] + 8 : ((N[2] + 3) & ~3) + 2 * GW_H;
+  if (need > P) return false;
   const size_t per_comp = (size_t)(GW_TX + 4) * (GW_TY + 4) * P * sizeof(float);
   const int fg = (int)std::min<size_t>(3, GW_SMEM_MAX / per_comp);
   if (fg < 1) return false;
@@ -495,13 +540,24 @@ static bool launch_gw_pitch(const float* coef, int ncomp, const float* disp, flo
     kern<<<grid, GW_NTH, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], sc);
   };
   if (FG == 3)
-    go(gather_win_kernel<3, GW_TX, GW_TY, GW_NTH, P>, 2);
+    go(gather_win_kernel<3, GW_TX, GW_TY, GW_NTH, P, SHIFT>, 2);
   else if (FG == 2)
-    go(gather_win_kernel<2, GW_TX, GW_TY, GW_NTH, P>, 1);
+    go(gather_win_kernel<2, GW_TX, GW_TY, GW_NTH, P, SHIFT>, 1);
   else
-    go(gather_win_kernel<1, GW_TX, GW_TY, GW_NTH, P>, 0);
+    go(gather_win_kernel<1, GW_TX, GW_TY, GW_NTH, P, SHIFT>, 0);
   LDDMM_LAUNCH_CHECK();
   return true;
+}
+
+template <bool SHIFT>
+static bool launch_gw_any(const float* coef, int ncomp, const float* disp, float* out, const int* N, float3 sc,
+                          cudaStream_t s) {
+  return launch_gw_pitch<64, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gw_pitch<128, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gw_pitch<192, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gw_pitch<264, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gw_pitch<392, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gw_pitch<520, SHIFT>(coef, ncomp, disp, out, N, sc, s);
 }
 
 void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float* out, const int* N,
@@ -509,17 +565,15 @@ void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float*
   launch_gather_scaled(coef, ncomp, disp, 1.f, 1.f, 1.f, out, N, s);
 }
 
-// Row pitch: the smallest compiled pitch >= Nz + 4 (multiple of 4); z rows
-// longer than 516 go to the tiled kernel (unit scale only).
+// Row pitch: the smallest compiled pitch holding the staged row (Nz + 8 with the
+// shifted groups when Nz % 4 == 0, else Nz + 4 rounded to 4); longer z rows go to
+// the tiled kernel (unit scale only).
 void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
                           const int* N, cudaStream_t s) {
   const float3 sc = make_float3(sx, sy, sz);
-  if (launch_gw_pitch<64>(coef, ncomp, disp, out, N, sc, s)) return;
-  if (launch_gw_pitch<128>(coef, ncomp, disp, out, N, sc, s)) return;
-  if (launch_gw_pitch<192>(coef, ncomp, disp, out, N, sc, s)) return;
-  if (launch_gw_pitch<264>(coef, ncomp, disp, out, N, sc, s)) return;
-  if (launch_gw_pitch<392>(coef, ncomp, disp, out, N, sc, s)) return;
-  if (launch_gw_pitch<520>(coef, ncomp, disp, out, N, sc, s)) return;
+  if (N[2] % 4 == 0 ? launch_gw_any<true>(coef, ncomp, disp, out, N, sc, s)
+                    : launch_gw_any<false>(coef, ncomp, disp, out, N, sc, s))
+    return;
   shape_require(sx == 1.f && sy == 1.f && sz == 1.f, "gather: z rows longer than 516 need unit scale");
   launch_gather_cubic_tiled(coef, ncomp, disp, out, N, s);
 }
