@@ -37,6 +37,9 @@ enum { LDDMM_OK = 0, LDDMM_ESHAPE = 1, LDDMM_EDIVERGENCE = 2, LDDMM_ECUDA = 3 };
 enum { LDDMM_ORIGINAL = 0, LDDMM_STATE_EQUATION = 1, LDDMM_DEFORMATION_STATE_EQUATION = 2 };
 /* Parameterization (core.hpp:271) */
 enum { LDDMM_STATIONARY = 0, LDDMM_NONSTATIONARY = 1 };
+/* Integrator (variants.hpp:35; note the reference enum order is {rk4, sl}: these
+ * values are the engine's, with the SL default at 0) */
+enum { LDDMM_SL = 0, LDDMM_RK4 = 1 };
 /* StopReason (optimizer.hpp:29-36), same order */
 enum {
   LDDMM_STOP_GRADIENT = 0,
@@ -51,8 +54,9 @@ typedef struct lddmm_ctx lddmm_ctx;
 
 /* Model<BandAlgebra> construction data: GridSpec (core.hpp:42-122), BandSpec
  * (spectral.hpp:22-83), Model fields variant/nt/sigma2/lop (variants.hpp:237-244),
- * SobolevOperator (spectral.hpp:518-525).  d = 3, band representation, SL
- * integrator; all three variants; stationary and nonstationary. */
+ * SobolevOperator (spectral.hpp:518-525), Model::integrator (variants.hpp:241).
+ * d = 3, band representation; SL-RK2 (default) or RK4 transport; all three
+ * variants; stationary and nonstationary. */
 typedef struct {
   int d;
   int dims[3];
@@ -64,6 +68,7 @@ typedef struct {
   double alpha;
   int s;
   double sigma2;
+  int integrator; /* LDDMM_SL or LDDMM_RK4 (RK4 needs nt >= 2, transport.hpp:236) */
 } lddmm_problem;
 
 /* ForwardCache energies + cfl (variants.hpp:196-198) */

@@ -405,6 +405,14 @@ class Provider:
             self._div[s] = band_divergence(self.node(i), self.b)
         return self._div[s]
 
+    def at(self, t):  # transport.hpp:141
+        return tv_sample(self.v, t, self.stationary)
+
+    def div_at(self, t):  # transport.hpp:164-172
+        if self.stationary:
+            return self.div_node(0)
+        return _lerp_nodes([self.div_node(i) for i in range(self.nt + 1)], min(max(t, 0.0), 1.0) * self.nt, self.nt)
+
     def departure(self, step, direction):  # transport.hpp:176-187
         key = (0 if self.stationary else step, direction)
         if key not in self._dep:
@@ -453,6 +461,54 @@ def sl_integrate(q_init, nt, direction, prov: Provider, src=None):
             raise Divergence(s)
         nodes[to] = nxt
     return nodes
+
+
+def rk4_integrate(q_init, nt, direction, rhs):
+    """transport.hpp:234-258 — classic RK4 on dq/dt = rhs(q, t) (Eulerian right-hand side)."""
+    if nt < 2:
+        raise ValueError("rk4 requires nt >= 2")
+    nodes = [None] * (nt + 1)
+    fwd = direction == "forward"
+    dt = 1.0 / nt if fwd else -1.0 / nt
+    at = 0 if fwd else nt
+    nodes[at] = q_init
+    for s in range(nt):
+        q = nodes[at]
+        t = at / nt
+        k1 = rhs(q, t)
+        k2 = rhs(0.5 * dt * k1 + q, t + 0.5 * dt)
+        k3 = rhs(0.5 * dt * k2 + q, t + 0.5 * dt)
+        k4 = rhs(dt * k3 + q, t + dt)
+        nxt = dt / 6.0 * k1 + (dt / 3.0 * k2 + (dt / 3.0 * k3 + (dt / 6.0 * k4 + q)))
+        if not np.all(np.isfinite(nxt)):
+            raise Divergence(s)
+        at += 1 if fwd else -1
+        nodes[at] = nxt
+    return nodes
+
+
+def _lerp_nodes(nodes, u, n):  # shared by sample (core.hpp:303-315) and sample_nodes (transport.hpp:44-54)
+    i = min(int(np.floor(u)), n - 1)
+    i = max(i, 0)
+    w = u - i
+    if w < 1e-14:
+        return nodes[i]
+    if w > 1.0 - 1e-14:
+        return nodes[i + 1]
+    return (1.0 - w) * nodes[i] + w * nodes[i + 1]
+
+
+def sample_nodes(nodes, t):  # transport.hpp:44-54 (t clamped to [0, 1])
+    n = len(nodes) - 1
+    return _lerp_nodes(nodes, min(max(t, 0.0), 1.0) * n, n)
+
+
+def tv_sample(v, t, stationary):  # TimeVaryingVelocity::sample (core.hpp:303-315)
+    if t < -1e-12 or t > 1.0 + 1e-12:
+        raise ValueError("sample: t outside [0,1]")
+    if stationary:
+        return v
+    return _lerp_nodes(v, t * (len(v) - 1), len(v) - 1)
 
 
 # ---------------------------------------------------------------------------
@@ -505,6 +561,7 @@ class Model:
     sigma2: float = 1.0
     lop: Sobolev = field(default_factory=Sobolev)
     stationary: bool = True
+    integrator: str = "sl"  # Model::integrator (variants.hpp:35,241): "sl" | "rk4"
 
     @property
     def grid(self):
@@ -659,45 +716,81 @@ class Model:
         r1 = (c.residual * (-2.0 / self.sigma2)) * c.grad_src_warped
         c.rho = self.solve_vector_continuity_backward(c.provider, project(r1, b))
 
-    # equation solvers, SL branches (variants.hpp:444-547)
+    # equation solvers (variants.hpp:444-547): SL gets the material source at nodes,
+    # RK4 the Eulerian right-hand side
     def solve_image_forward(self, pv, m0):
-        return sl_integrate(m0, self.nt, "forward", pv, None)
+        if self.integrator == "sl":
+            return sl_integrate(m0, self.nt, "forward", pv, None)
+        b = self.band
+        return rk4_integrate(m0, self.nt, "forward",
+                             lambda q, t: -1.0 * star_dot(band_gradient(q, b), pv.at(t), b))
 
     def solve_scalar_continuity_backward(self, pv, q1):
         b = self.band
-        return sl_integrate(q1, self.nt, "backward", pv, lambda q, i: -1.0 * star(q, pv.div_node(i), b))
+        if self.integrator == "sl":
+            return sl_integrate(q1, self.nt, "backward", pv, lambda q, i: -1.0 * star(q, pv.div_node(i), b))
+        return rk4_integrate(q1, self.nt, "backward", lambda q, t: -1.0 * (
+            1.0 * star(q, pv.div_at(t), b) + star_dot(band_gradient(q, b), pv.at(t), b)))
 
     def solve_displacement(self, pv, direction):
+        b = self.band
         z = np.zeros((self.grid.d,) + self.band.bounds, dtype=np.complex128)
-        return sl_integrate(z, self.nt, direction, pv, lambda q, i: pv.node(i).copy())
+        if self.integrator == "sl":
+            return sl_integrate(z, self.nt, direction, pv, lambda q, i: pv.node(i).copy())
+
+        def rhs(q, t):
+            vt = pv.at(t)
+            return -1.0 * band_jac_mul(q, vt, b) + vt
+        return rk4_integrate(z, self.nt, direction, rhs)
 
     def solve_jacobian_factor(self, pv):
         b = self.band
         z = np.zeros(self.band.bounds, dtype=np.complex128)
+        if self.integrator == "sl":
+            def src(q, i):
+                dvv = pv.div_node(i)
+                return -1.0 * star(q, dvv, b) + dvv
+            return sl_integrate(z, self.nt, "backward", pv, src)
 
-        def src(q, i):
-            dvv = pv.div_node(i)
-            return -1.0 * star(q, dvv, b) + dvv
-        return sl_integrate(z, self.nt, "backward", pv, src)
+        def rhs(q, t):
+            dvv = pv.div_at(t)
+            return -1.0 * star_dot(band_gradient(q, b), pv.at(t), b) + (-1.0 * star(q, dvv, b) + dvv)
+        return rk4_integrate(z, self.nt, "backward", rhs)
 
     def solve_vector_continuity_backward(self, pv, q1):
         b = self.band
-        return sl_integrate(q1, self.nt, "backward", pv, lambda q, i: -1.0 * star(pv.div_node(i), q, b))
+        if self.integrator == "sl":
+            return sl_integrate(q1, self.nt, "backward", pv, lambda q, i: -1.0 * star(pv.div_node(i), q, b))
+        return rk4_integrate(q1, self.nt, "backward", lambda q, t: -1.0 * (
+            1.0 * star(pv.div_at(t), q, b) + band_jac_mul(q, pv.at(t), b)))
 
     def solve_incremental_image(self, pv, gm, dv):
         b = self.band
         z = np.zeros(self.band.bounds, dtype=np.complex128)
-        return sl_integrate(z, self.nt, "forward", pv,
-                            lambda q, i: -1.0 * star_dot(gm[i], self.tv_node(dv, i), b))
+        if self.integrator == "sl":
+            return sl_integrate(z, self.nt, "forward", pv,
+                                lambda q, i: -1.0 * star_dot(gm[i], self.tv_node(dv, i), b))
+
+        def rhs(q, t):
+            gmt = sample_nodes(gm, t)
+            return -1.0 * (1.0 * star_dot(gmt, tv_sample(dv, t, self.stationary), b)
+                           + star_dot(band_gradient(q, b), pv.at(t), b))
+        return rk4_integrate(z, self.nt, "forward", rhs)
 
     def solve_incremental_displacement(self, pv, u, dv):
         b = self.band
         z = np.zeros((self.grid.d,) + self.band.bounds, dtype=np.complex128)
+        if self.integrator == "sl":
+            def src(q, i):
+                dvi = self.tv_node(dv, i)
+                return -1.0 * band_jac_mul(u[i], dvi, b) + dvi
+            return sl_integrate(z, self.nt, "forward", pv, src)
 
-        def src(q, i):
-            dvi = self.tv_node(dv, i)
-            return -1.0 * band_jac_mul(u[i], dvi, b) + dvi
-        return sl_integrate(z, self.nt, "forward", pv, src)
+        def rhs(q, t):
+            dvt = tv_sample(dv, t, self.stationary)
+            ut = sample_nodes(u, t)
+            return -1.0 * band_jac_mul(q, pv.at(t), b) + (-1.0 * band_jac_mul(ut, dvt, b) + dvt)
+        return rk4_integrate(z, self.nt, "forward", rhs)
 
 
 # ---------------------------------------------------------------------------

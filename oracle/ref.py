@@ -225,7 +225,7 @@ class RefModel:
     """Model<BandAlgebra> of the reference (variants.hpp:229-548), SL integrator."""
 
     def __init__(self, I0, I1, dims, spacing, band, variant="deformation_state_equation", nt=5,
-                 sigma2=1.0, alpha=0.0025, s=2, param="stationary"):
+                 sigma2=1.0, alpha=0.0025, s=2, param="stationary", integrator="sl"):
         self.dims, self.spacing, self.band = tuple(dims), tuple(spacing), tuple(band)
         self.d = len(dims)
         self.nt = nt
@@ -239,6 +239,8 @@ class RefModel:
         if not h:
             raise RefError(lib().ref_last_error().decode())
         self.h = C.c_void_p(h)
+        if integrator != "sl":
+            _check(lib().ref_model_set_integrator(self.h, 1 if integrator == "rk4" else 0), "set_integrator")
 
     def __del__(self):
         if getattr(self, "h", None):

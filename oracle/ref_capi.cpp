@@ -256,6 +256,11 @@ void* ref_model_create(int d, const int* dims, const double* h, const int* band,
 
 void ref_model_destroy(void* h) { delete static_cast<RefModel*>(h); }
 
+// Model::integrator (variants.hpp:35,241): 0 sl, 1 rk4
+int ref_model_set_integrator(void* h, int rk4) {
+  return guard([&] { static_cast<RefModel*>(h)->model->integrator = rk4 ? Integrator::rk4 : Integrator::sl; });
+}
+
 // energies[4] = {E, E_reg, E_data, cfl}
 int ref_model_forward(void* h, const double* v, int with_adjoint, double* energies, int* step) {
   auto* m = static_cast<RefModel*>(h);

@@ -122,6 +122,8 @@ int lddmm_create(const lddmm_problem* p, int device, lddmm_ctx** out) {
     q.alpha = p->alpha;
     q.s = p->s;
     q.sigma2 = p->sigma2;
+    shape_require(p->integrator == LDDMM_SL || p->integrator == LDDMM_RK4, "unknown integrator");
+    q.rk4 = p->integrator == LDDMM_RK4 ? 1 : 0;
     ctx->eng = std::make_unique<Engine>(q, device);
   });
   if (rc != LDDMM_OK) {

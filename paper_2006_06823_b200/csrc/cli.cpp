@@ -8,8 +8,8 @@
 // warps, Jacobians and Dice counts run on the GPU through liblddmm_cuda.so;
 // this file only parses arguments, reads/writes files and formats reports.
 //
-// Scope: the engine is the band-limited SL path on 3-D grids.  --repr spatial,
-// --integrator rk4 and 2-D registrations exit with status 1 and say so
+// Scope: the band representation on 3-D grids, SL-RK2 or RK4 transport.
+// --repr spatial and 2-D registrations exit with status 1 and say so
 // (SURVEY.md §8f4).  `synth` generates 2-D and 3-D blobs/discs fixtures with
 // the reference's seeded generators (synth.hpp:20-42,182-259) restated here.
 #include <algorithm>
@@ -360,14 +360,16 @@ int do_register(const RegOpts& o) {
   else throw InputError("unknown parameterization: " + o.param);
   if (o.repr != "band" && o.repr != "bl" && o.repr != "spatial")
     throw InputError("unknown representation: " + o.repr + " (expected spatial or band)");
-  if (o.repr == "spatial" || o.integrator == "rk4")
-    throw InputError("--repr spatial / --integrator rk4 are not part of the B200 engine (band SL path only)");
+  if (o.repr == "spatial")
+    throw InputError("--repr spatial is not part of the B200 engine (band representation only)");
   if (!(o.band >= 4 && o.band % 2 == 0)) throw InputError("--band must be even and >= 4");
   require_3d(I0.grid);
   const Grid& g = I0.grid;
   const std::size_t N = g.size();
 
-  Ctx ctx(problem_for(g, o.band, nt, variant, param, o.alpha, o.s, o.sigma2));
+  lddmm_problem prob = problem_for(g, o.band, nt, variant, param, o.alpha, o.s, o.sigma2);
+  prob.integrator = o.integrator == "rk4" ? LDDMM_RK4 : LDDMM_SL;
+  Ctx ctx(prob);
   ctx.check(lddmm_set_images(ctx.h, I0.v.data(), I1.v.data()));
   double* v = nullptr;
   ctx.check(lddmm_vel_alloc(ctx.h, &v));

@@ -53,6 +53,7 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   shape_require(p.nt >= 1, "nt must be >= 1");
   shape_require(p.alpha > 0.0 && p.s >= 1, "sobolev: alpha > 0 and s >= 1 required");
   shape_require(p.variant >= 0 && p.variant <= 2, "unknown variant");
+  shape_require(!p.rk4 || p.nt >= 2, "rk4 requires nt >= 2");
   LDDMM_CUDA(cudaSetDevice(device));
   // A blocking stream: it is ordered against the legacy default stream, so device
   // buffers a caller fills or allocates there (torch tensors, cudaMemset) are
@@ -104,9 +105,9 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   for (ProviderState* ps : {&prov_, &trial_prov_}) {
     ps->v.alloc(nodes() * V);
     ps->div.alloc(nodes() * kprod());
-    ps->dep_fwd.alloc(nsteps * 3 * N);
+    if (!p.rk4) ps->dep_fwd.alloc(nsteps * 3 * N);  // RK4 never samples departure points
   }
-  prov_.dep_bwd.alloc(nsteps * 3 * N);
+  if (!p.rk4) prov_.dep_bwd.alloc(nsteps * 3 * N);
   if (!p.stationary) pscratch_.alloc(9 * N);
   u_.alloc((p.nt + 1) * V);
   rho_.alloc((p.nt + 1) * V);
@@ -114,6 +115,7 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   dseries_.alloc((p.nt + 1) * V);
   tmp_u_.alloc(2 * V);
   btmp_.alloc(12 * V);
+  if (p.rk4) rk_.alloc(12 * V);
   m1_.alloc(4 * N);  // m1 followed by grad_src_warped [3][N]
   res_.alloc(N);
   ugrid_.alloc(3 * N);
@@ -479,7 +481,10 @@ void Engine::provider_build(const double2* v, ProviderState& ps, bool with_bwd) 
     const int g = launch_absmax_partial(3 * N, dst, part_.p, stream_);
     launch_reduce_final(part_, g, 1, slots_.p + 16 + i, stream_);  // cfl: max over nodes (transport.hpp:189-194)
   };
-  if (prob_.stationary) {
+  if (prob_.rk4) {
+    // RK4 uses the band velocity and divergence only; iota(v_i) is embedded for the cfl
+    for (int i = 0; i < nn; ++i) embed_node(i, gridA_.p);
+  } else if (prob_.stationary) {
     embed_node(0, gridA_.p);
     launch_departure(gridA_.p, gridA_.p + 3 * N, dt, h_, ps.dep_fwd.p, with_bwd ? ps.dep_bwd.p : nullptr, gridB_.p,
                      full_.N, stream_);
@@ -510,6 +515,7 @@ void Engine::provider_build(const double2* v, ProviderState& ps, bool with_bwd) 
 }
 
 void Engine::departure(const double2* v, float* dep_fwd, float* dep_bwd, double* cfl) {
+  shape_require(!prob_.rk4, "departure points belong to the SL integrator");
   provider_build(v, prov_, true);
   const long long N = npts();
   if (dep_fwd)
@@ -550,6 +556,10 @@ void Engine::check_series_finite(const double2* series, int count, int first, bo
 // D_t u = v forward from 0 (variants.hpp:468-472) with the stationary f_from
 // cached: next = dt/2 f_from + (dt/2 v + A), A = advect(u_s) (A = 0 at s = 0).
 void Engine::solve_displacement_fwd(ProviderState& ps, double2* series, bool keep_all, double2* last) {
+  if (prob_.rk4) {
+    rk4_displacement(ps, true, keep_all ? series : nullptr, last);
+    return;
+  }
   const long long V = vec_elems(), K = kprod();
   const int nt = prob_.nt;
   const double dt = 1.0 / nt;
@@ -590,6 +600,10 @@ void Engine::solve_displacement_fwd(ProviderState& ps, double2* series, bool kee
 
 // componentwise continuity D_t q = -(div v) q, backward from q1 (variants.hpp:499-503)
 void Engine::solve_vector_continuity_bwd(ProviderState& ps, const double2* q1, double2* series) {
+  if (prob_.rk4) {
+    rk4_vector_continuity_bwd(ps, q1, series);
+    return;
+  }
   const long long V = vec_elems(), K = kprod();
   const int nt = prob_.nt;
   const double sdt = -1.0 / nt;
@@ -617,6 +631,10 @@ void Engine::solve_vector_continuity_bwd(ProviderState& ps, const double2* q1, d
 // D_t du = dv - (Du) dv forward from 0 (variants.hpp:530-540), merged advect:
 // next = advect(du_s + dt/2 src_s) + dt/2 src_{s+1}.
 void Engine::solve_incremental_displacement(ProviderState& ps, const double2* dv, double2* series) {
+  if (prob_.rk4) {
+    rk4_incremental_displacement(ps, dv, series);
+    return;
+  }
   const long long V = vec_elems(), K = kprod();
   const int nt = prob_.nt;
   const double dt = 1.0 / nt;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -21,6 +22,7 @@ struct Problem {
   int nt = 5;
   int variant = 2;     // 0 original, 1 state_equation, 2 deformation_state_equation (variants.hpp:34)
   int stationary = 1;  // Parameterization (core.hpp:271)
+  int rk4 = 0;         // Integrator: 0 SL-RK2, 1 RK4 (variants.hpp:35,241)
   double alpha = 0.0025;
   int s = 2;
   double sigma2 = 1.0;
@@ -241,6 +243,23 @@ class Engine {
   double2* node(DevBuf<double2>& s, int i) const { return s.p + (long long)i * vec_elems(); }
 
   void provider_build(const double2* v, ProviderState& ps, bool with_bwd);
+  // ---- RK4 integrator (transport.hpp:234-258), band representation (rk4.cu) ----
+  using RkRhs = std::function<void(const double2* q, double t, double2* out)>;
+  void rk4_run(long long C, const double2* init, double2* series, double2* last, bool forward, const RkRhs& rhs);
+  const double2* rk_vel_at(const ProviderState& ps, double t, double2* scratch);
+  const double2* rk_div_at(const ProviderState& ps, double t, double2* scratch);
+  const double2* rk_tv_at(const double2* tv, double t, double2* scratch);
+  const double2* rk_series_at(const double2* series, long long C, double t, double2* scratch);
+  void graddot(const double2* q, const double2* w, double2* out, double alpha, const double2* add, double beta);
+  double2* rk(int i) const { return rk_.p + (long long)i * vec_elems(); }
+  DevBuf<double2> rk_;  // RK4 stages and samples: 12 band vectors
+  void enqueue_finite(const double2* p, long long n, int step);
+  void rk4_displacement(ProviderState& ps, bool forward, double2* series, double2* last);
+  void rk4_vector_continuity_bwd(ProviderState& ps, const double2* q1, double2* series);
+  void rk4_incremental_displacement(ProviderState& ps, const double2* dv, double2* series);
+  void rk4_image_forward(ProviderState& ps, const double2* m0, double2* series, double2* last);
+  void rk4_scalar_continuity_bwd(ProviderState& ps, const double2* q1, double2* series, bool jf);
+  void rk4_incremental_image(ProviderState& ps, const double2* dv, double2* series);
   void solve_displacement_fwd(ProviderState& ps, double2* series, bool keep_all, double2* last);
   void solve_vector_continuity_bwd(ProviderState& ps, const double2* q1, double2* series);
   void solve_incremental_displacement(ProviderState& ps, const double2* dv, double2* series);

@@ -47,6 +47,10 @@ void Engine::ensure_variant_buffers() {
 
 // D_t u = v forward (from 0 at t = 0) or backward (from 0 at t = 1), variants.hpp:468-472
 void Engine::solve_displacement(ProviderState& ps, bool forward, double2* series) {
+  if (prob_.rk4) {
+    rk4_displacement(ps, forward, series, nullptr);
+    return;
+  }
   const long long V = vec_elems(), K = kprod();
   const int nt = prob_.nt;
   const double sdt = forward ? 1.0 / nt : -1.0 / nt;
@@ -85,6 +89,10 @@ void Engine::solve_displacement(ProviderState& ps, bool forward, double2* series
 // D_t m = 0 forward from m0 (variants.hpp:444-446): m_{s+1} = advect(m_s)
 void Engine::solve_image_forward(ProviderState& ps, const double2* m0, double2* series, bool keep_all,
                                  double2* last) {
+  if (prob_.rk4) {
+    rk4_image_forward(ps, m0, keep_all ? series : nullptr, last);
+    return;
+  }
   const long long S = kprod();
   const int nt = prob_.nt;
   const double2* prev = m0;
@@ -107,6 +115,10 @@ void Engine::solve_image_forward(ProviderState& ps, const double2* m0, double2* 
 // Backward SL with source src(q) = -(q * div v) [+ div v for the Jacobian factor]
 // (variants.hpp:454-457 scalar continuity, 482-489 jacobian factor)
 void Engine::solve_scalar_continuity_bwd(ProviderState& ps, const double2* q1, double2* series, bool jf) {
+  if (prob_.rk4) {
+    rk4_scalar_continuity_bwd(ps, q1, series, jf);
+    return;
+  }
   const long long S = kprod();
   const int nt = prob_.nt;
   const double sdt = -1.0 / nt;
@@ -148,6 +160,10 @@ void Engine::small_custom(const PrepArgs& pa, int prodop, double2* out, int nout
 
 // D_t dm = -grad(m_i) . dv, forward from 0 (variants.hpp:512-519), merged advect
 void Engine::solve_incremental_image(ProviderState& ps, const double2* dv, double2* series) {
+  if (prob_.rk4) {
+    rk4_incremental_image(ps, dv, series);
+    return;
+  }
   const long long S = kprod(), K = kprod();
   const int nt = prob_.nt;
   const double dt = 1.0 / nt;

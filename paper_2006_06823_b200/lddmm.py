@@ -44,7 +44,10 @@ class CudaError(RuntimeError):
 class _Problem(C.Structure):
     _fields_ = [("d", C.c_int), ("dims", C.c_int * 3), ("spacing", C.c_double * 3), ("band", C.c_int * 3),
                 ("nt", C.c_int), ("variant", C.c_int), ("parameterization", C.c_int), ("alpha", C.c_double),
-                ("s", C.c_int), ("sigma2", C.c_double)]
+                ("s", C.c_int), ("sigma2", C.c_double), ("integrator", C.c_int)]
+
+
+INTEGRATORS = {"sl": 0, "rk4": 1}  # include/lddmm_cuda.h LDDMM_SL / LDDMM_RK4
 
 
 class _Energies(C.Structure):
@@ -252,7 +255,7 @@ class Context:
     """One engine context (device memory + stream) for one registration problem."""
 
     def __init__(self, band: BandSpec, variant="deformation_state_equation", nt=5, sigma2=1.0,
-                 lop: SobolevOperator = None, parameterization="stationary", device=0):
+                 lop: SobolevOperator = None, parameterization="stationary", device=0, integrator="sl"):
         lop = lop or SobolevOperator()
         g = band.parent
         if g.d != 3:
@@ -269,6 +272,9 @@ class Context:
         p.alpha = lop.alpha
         p.s = lop.s
         p.sigma2 = sigma2
+        if integrator not in INTEGRATORS:
+            raise ShapeError(f"unknown integrator: {integrator} (expected sl or rk4)")
+        p.integrator = INTEGRATORS[integrator]
         h = C.c_void_p()
         rc = lib().lddmm_create(C.byref(p), int(device), C.byref(h))
         if rc != 0:
@@ -357,11 +363,13 @@ class Velocity:
 
 
 class Model:
-    """Model<BandAlgebra> with the SL integrator (variants.hpp:229-548) on one B200."""
+    """Model<BandAlgebra> (variants.hpp:229-548) on one B200; integrator "sl" (SL-RK2,
+    the default) or "rk4" (transport.hpp:234-258)."""
 
     def __init__(self, band: BandSpec, source, target, variant="deformation_state_equation", nt=5, sigma2=1.0,
-                 lop: SobolevOperator = None, parameterization="stationary", device=0):
-        self.ctx = Context(band, variant, nt, sigma2, lop, parameterization, device)
+                 lop: SobolevOperator = None, parameterization="stationary", device=0, integrator="sl"):
+        self.ctx = Context(band, variant, nt, sigma2, lop, parameterization, device, integrator)
+        self.integrator = integrator
         self.band, self.variant, self.nt, self.sigma2 = band, variant, nt, sigma2
         self.lop = lop or SobolevOperator()
         self.set_images(source, target)

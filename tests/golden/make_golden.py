@@ -182,6 +182,35 @@ def cli_register():
                         iterations=r["iterations"], jac=jac, dice_mean=e["dice_mean"], v=r["v"])
 
 
+def model_rk4():
+    """RK4 integrator (transport.hpp:234-258; variants.hpp:444-547 rk4 branches), band
+    representation, all three variants, stationary and nonstationary (§8f row 4)."""
+    dims, h, band, nt = (16, 12, 14), (1.0, 1.0, 1.0), (8, 8, 6), 4
+    I0 = ref.random_smooth_image(dims, h, 91, 1.0)
+    I1 = ref.random_smooth_image(dims, h, 92, 1.0)
+    v = ref.random_band_field(dims, h, band, 93, 1.0, 2.0)[None]
+    dv = ref.random_band_field(dims, h, band, 94, 1.0, 2.0)[None]
+    vn = np.stack([ref.random_band_field(dims, h, band, 95 + i, 1.0, 2.0) for i in range(nt + 1)])
+    dvn = np.stack([ref.random_band_field(dims, h, band, 105 + i, 1.0, 2.0) for i in range(nt + 1)])
+    out = dict(dims=np.array(dims), band=np.array(band), nt=nt, sigma2=0.5, I0=I0, I1=I1, v=v, dv=dv, vn=vn, dvn=dvn)
+    for var in ("deformation_state_equation", "original", "state_equation"):
+        for tag, param, vv, dd in (("s", "stationary", v, dv), ("n", "nonstationary", vn, dvn)):
+            m = ref.RefModel(I0, I1, dims, h, band, var, nt, 0.5, param=param, integrator="rk4")
+            e = m.forward(vv, True)
+            out[f"{var}_{tag}_energy"] = np.array([e["energy"], e["energy_reg"], e["energy_data"], e["cfl"]])
+            out[f"{var}_{tag}_gradient"] = m.gradient()
+            out[f"{var}_{tag}_hessvec"] = m.hessvec(dd)
+        m = ref.RefModel(I0, I1, dims, h, band, var, nt, 0.5, integrator="rk4")
+        r = m.optimize(None, max_iter=3)
+        out[f"{var}_opt_history"] = np.array([[q.iter, q.energy, q.pcg_iters, q.epsilon] for q in r["history"]])
+        out[f"{var}_opt_stop"] = ref.STOP_REASONS.index(r["stop"])
+        out[f"{var}_opt_v"] = r["v"]
+    m = ref.RefModel(I0, I1, dims, h, band, "deformation_state_equation", nt, 0.5, integrator="rk4")
+    fwd, inv, jac = m.maps(v)
+    out["maps_fwd"], out["maps_inv"], out["maps_jac"] = fwd, inv, jac
+    np.savez_compressed(os.path.join(HERE, "model_rk4.npz"), **out)
+
+
 if __name__ == "__main__":
     if not ref.available():
         sys.exit("build oracle/_ref first: make -C oracle ref")
@@ -194,6 +223,7 @@ if __name__ == "__main__":
     synth()
     evaluation()
     cli_register()
+    model_rk4()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

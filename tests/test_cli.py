@@ -65,7 +65,7 @@ def test_usage_and_input_errors(tmp_path):
     r = run("register", "--source", str(tmp_path / "nope.raw"), "--target", str(tmp_path / "nope.raw"),
             "--out", str(tmp_path / "o"))
     assert r.returncode == 1 and "cannot open sidecar" in r.stderr
-    # 2-D inputs and the spatial / rk4 paths are outside the engine: status 1 with a reason
+    # 2-D inputs and the spatial representation are outside the engine: status 1 with a reason
     assert run("synth", "--kind", "blobs", "--n", "16", "--out", str(tmp_path / "b2")).returncode == 0
     r = run("register", "--source", str(tmp_path / "b2" / "source.raw"), "--target",
             str(tmp_path / "b2" / "target.raw"), "--out", str(tmp_path / "o2"))

@@ -152,3 +152,17 @@ def test_cli_nonstationary_outputs(cuda, tmp_path):
         assert (tmp_path / "r" / f"velocity_{i:02d}.raw").exists()
     with open(tmp_path / "r" / "report.json") as f:
         assert json.load(f)["parameterization"] == "nonstationary"
+
+
+def test_cli_rk4(cuda, tmp_path):
+    """--integrator rk4 on the band representation (lddmm_cli.cpp:216-218: nt defaults to 25)."""
+    assert run("synth", "--kind", "blobs", "--d", "3", "--n", "16", "--seed", "3", "--out",
+               str(tmp_path / "b")).returncode == 0
+    r = run("register", "--source", str(tmp_path / "b" / "source.raw"), "--target",
+            str(tmp_path / "b" / "target.raw"), "--out", str(tmp_path / "r"), "--integrator", "rk4",
+            "--band", "8", "--max-iter", "2", "--variant", "deformation_state_equation", "--sigma2", "0.01")
+    assert r.returncode == 0, r.stderr
+    with open(tmp_path / "r" / "report.json") as f:
+        rep = json.load(f)
+    assert rep["integrator"] == "rk4" and rep["nt"] == 25
+    assert rep["mse_rel_final"] < rep["mse_rel_initial"]

@@ -6,12 +6,16 @@ linearity) and test_optimizer.cpp (descent, stop rules) at sizes the oracle
 finishes in seconds.  Tolerances: energies rel 1e-5, band vectors
 rel-L2 1e-4, GN/PCG iteration counts and stop reason identical.
 """
+import os
+
 import numpy as np
 import pytest
 
 from oracle import lddmm_np as O
 
 pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def rel(a, b):
@@ -183,3 +187,48 @@ def test_nonstationary_model_and_optimize(cuda, variant):
         assert r.pcg_iters == q["pcg_iters"] and r.epsilon == q["epsilon"]
         assert abs(r.energy - q["energy"]) <= 1e-5 * abs(q["energy"])
     assert rel(res.v.numpy(), np.stack(ref["v"])) < 1e-4
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("tag", ["s", "n"])
+def test_rk4_matches_reference(cuda, variant, tag):
+    """RK4 integrator on the device (transport.hpp:234-258, rk4 branches of
+    variants.hpp:444-547) against the reference's own outputs (tests/golden/model_rk4.npz):
+    forward energies, gradient, hessvec (stationary and nonstationary), a short optimize
+    with identical GN/PCG path, and the endpoint maps."""
+    from paper_2006_06823_b200 import lddmm as L
+    z = np.load(os.path.join(GOLD, "model_rk4.npz"))
+    dims = tuple(int(x) for x in z["dims"])
+    band, nt = tuple(int(x) for x in z["band"]), int(z["nt"])
+    st = tag == "s"
+    gm = L.Model(L.BandSpec(L.GridSpec(dims), band), z["I0"], z["I1"], variant, nt, float(z["sigma2"]),
+                 parameterization="stationary" if st else "nonstationary", integrator="rk4")
+    v = z["v"] if st else z["vn"]
+    dv = z["dv"] if st else z["dvn"]
+    e = gm.forward(gm.velocity(v), True)
+    ref = z[f"{variant}_{tag}_energy"]
+    assert abs(e["energy"] - ref[0]) <= 1e-5 * abs(ref[0])
+    assert abs(e["energy_reg"] - ref[1]) <= 1e-9 * abs(ref[1])
+    assert abs(e["cfl"] - ref[3]) <= 1e-5 * ref[3]
+    assert rel(gm.gradient().numpy(), z[f"{variant}_{tag}_gradient"]) < 1e-4
+    assert rel(gm.hessvec(gm.velocity(dv)).numpy(), z[f"{variant}_{tag}_hessvec"]) < 1e-4
+    if st:
+        res = L.optimize(gm, None, L.OptimizeOptions(max_iter=3))
+        hist = z[f"{variant}_opt_history"]
+        assert L.STOP_REASONS.index(res.stop) == int(z[f"{variant}_opt_stop"])
+        assert len(res.history) == hist.shape[0]
+        for r, row in zip(res.history, hist):
+            assert r.pcg_iters == int(row[2]) and r.epsilon == row[3]
+            assert abs(r.energy - row[1]) <= 1e-5 * abs(row[1])
+        assert rel(res.v.numpy(), z[f"{variant}_opt_v"]) < 1e-4
+    if st and variant == "deformation_state_equation":
+        f, i, jac = L.compute_maps(gm, gm.velocity(v))
+        assert rel(f, z["maps_fwd"]) < 1e-4 and rel(i, z["maps_inv"]) < 1e-4
+        assert np.allclose(jac, z["maps_jac"], atol=1e-4)
+
+
+def test_rk4_needs_two_steps(cuda):
+    """rk4_integrate rejects nt < 2 (transport.hpp:236) — ShapeError at context creation."""
+    from paper_2006_06823_b200 import lddmm as L
+    with pytest.raises(L.ShapeError):
+        L.Context(L.BandSpec(L.GridSpec((8, 8, 8)), (4, 4, 4)), nt=1, integrator="rk4")

@@ -201,3 +201,38 @@ def test_evaluation_golden():
     det = O.map_jacobian_determinant(z["disp"], g)
     assert np.max(np.abs(det - z["det"])) < 1e-12
     assert np.allclose([det.min(), det.max()], z["jac"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("variant", ["deformation_state_equation", "original", "state_equation"])
+@pytest.mark.parametrize("tag", ["s", "n"])
+def test_model_rk4_golden(variant, tag):
+    """RK4 integrator (transport.hpp:234-258, the rk4 branches of variants.hpp:444-547),
+    band representation, stationary (s) and nonstationary (n), against the reference."""
+    z = load("model_rk4")
+    dims = tuple(int(x) for x in z["dims"])
+    g = O.Grid(dims, (1.0, 1.0, 1.0))
+    b = O.Band(g, tuple(int(x) for x in z["band"]))
+    nt = int(z["nt"])
+    st = tag == "s"
+    m = O.Model(b, z["I0"], z["I1"], variant, nt, float(z["sigma2"]), stationary=st, integrator="rk4")
+    v = z["v"][0] if st else list(z["vn"])
+    dv = z["dv"][0] if st else list(z["dvn"])
+    c = m.forward(v, True)
+    assert np.allclose([c.energy, c.energy_reg, c.energy_data, c.cfl], z[f"{variant}_{tag}_energy"], rtol=1e-12)
+    gr = m.gradient(c)
+    hv = m.hessvec(c, dv)
+    gw, hw = z[f"{variant}_{tag}_gradient"], z[f"{variant}_{tag}_hessvec"]
+    assert rel(gr if st else np.stack(gr), gw[0] if st else gw) < 1e-11
+    assert rel(hv if st else np.stack(hv), hw[0] if st else hw) < 1e-11
+    if st:
+        r = O.optimize(m, m.zero_velocity(), O.Options(max_iter=3))
+        hist = z[f"{variant}_opt_history"]
+        assert O.STOP.index(r["stop"]) == int(z[f"{variant}_opt_stop"])
+        assert len(r["history"]) == hist.shape[0]
+        for q, row in zip(r["history"], hist):
+            assert q["pcg_iters"] == int(row[2]) and q["epsilon"] == row[3]
+            assert abs(q["energy"] - row[1]) <= 1e-9 * abs(row[1])
+        assert rel(r["v"], z[f"{variant}_opt_v"][0]) < 1e-8
+    if st and variant == "deformation_state_equation":
+        fwd, inv = O.compute_maps(m, v)
+        assert rel(fwd, z["maps_fwd"]) < 1e-12 and rel(inv, z["maps_inv"]) < 1e-12
