@@ -103,7 +103,7 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_cost(threads=1, dims=DIMS, band=BAND, nt=NT, measured=None):
+def cpu_reference_cost(threads=1, dims=DIMS, band=BAND, nt=NT, measured=None, source="our run"):
     """Reference CPU s/registration for the same workload (see module doc).  measured =
     (forwards, hessvecs, trials) of our run gives the identical operation sequence;
     without it the nominal budget GN x PCG x 1 trial is used."""
@@ -114,7 +114,8 @@ def cpu_reference_cost(threads=1, dims=DIMS, band=BAND, nt=NT, measured=None):
     sample_s = time.time() - t0
     if measured is not None:
         counts = ref.defstate_op_counts_measured(nt, *measured)
-        how = f"the measured op sequence of our run ({measured[0]} forwards+gradients, {measured[1]} hessvecs, {measured[2]} trials)"
+        how = (f"the measured op sequence of {source} ({measured[0]} forwards+gradients, {measured[1]} hessvecs, "
+               f"{measured[2]} trials)")
     else:
         counts = ref.defstate_op_counts(nt, GN, PCG, 1)
         how = f"the nominal budget {GN} GN x {PCG} PCG x 1 trial"
@@ -128,6 +129,21 @@ def cpu_reference_cost(threads=1, dims=DIMS, band=BAND, nt=NT, measured=None):
     return ms / 1000.0, sample
 
 
+def reference_op_sequence():
+    """(forwards, hessvecs, trials) of the reference's own config-2 registration, read
+    from its GN history (tests/golden/config2_ref.npz: 3 GN iterations, PCG 2+3+4,
+    epsilon 1 each): forward+gradient per history row, one hessvec per PCG iteration,
+    log2(1/epsilon) + 1 Armijo trials per iteration.  None if the fixture is absent."""
+    path = os.path.join(ROOT, "tests", "golden", "config2_ref.npz")
+    if not os.path.exists(path):
+        return None
+    h = np.load(path)["history"]
+    forwards = int(h.shape[0])
+    hessvecs = int(np.sum(h[1:, 6]))
+    trials = int(sum(1 + round(np.log2(1.0 / e)) for e in h[1:, 8] if e > 0))
+    return forwards, hessvecs, trials
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -136,10 +152,12 @@ def run_reference(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_lddmm.so not built"}))
         return
     threads = os.cpu_count() or 1
+    measured = reference_op_sequence()
     vals = []
     sample = ""
     for _ in range(max(1, args.steps)):
-        v, sample = cpu_reference_cost(threads)
+        v, sample = cpu_reference_cost(threads, measured=measured,
+                                       source="the reference's own config-2 run (tests/golden/config2_ref.npz)")
         vals.append(v)
     value = float(np.mean(vals))
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s/registration", "n_gpus": args.gpus,
