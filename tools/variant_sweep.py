@@ -16,11 +16,12 @@ dims = tuple(int(x) for x in os.environ.get("DIMS", "180,210,180").split(","))
 K = int(os.environ.get("BAND", "32"))
 nt = int(os.environ.get("NT", "10"))
 reps = int(os.environ.get("REPS", "2"))
+integ = os.environ.get("INTEGRATOR", "sl")
 I0, I1 = phantoms.brain_pair(dims)
 d0 = torch.from_numpy(I0).cuda().float()
 d1 = torch.from_numpy(I1).cuda().float()
 for variant in ("deformation_state_equation", "original", "state_equation"):
-    m = L.Model(L.BandSpec(L.GridSpec(dims), (K, K, K)), d0, d1, variant, nt, 0.01)
+    m = L.Model(L.BandSpec(L.GridSpec(dims), (K, K, K)), d0, d1, variant, nt, 0.01, integrator=integ)
     opt = L.OptimizeOptions(max_iter=10, pcg_max_iter=5)
     times = []
     for r in range(reps + 1):
@@ -35,5 +36,5 @@ for variant in ("deformation_state_equation", "original", "state_equation"):
                       "iterations": res.iterations, "hessvecs": res.hessvecs, "trials": res.trials,
                       "pcg": [h.pcg_iters for h in res.history[1:]],
                       "mse_rel_final": res.history[-1].mse_rel, "jacobian": list(jac),
-                      "dims": dims, "band": K, "nt": nt}))
+                      "dims": dims, "band": K, "nt": nt, "integrator": integ}))
     del m
