@@ -211,6 +211,30 @@ def model_rk4():
     np.savez_compressed(os.path.join(HERE, "model_rk4.npz"), **out)
 
 
+def gate8():
+    """Acceptance gate 8 analog in 3-D (acceptance.cpp:307-343): two-disc cases at 32^3,
+    K = 16, SL nt = 5, sigma2 = 0.05, max_iter 30, grad_tol 1e-3; mean Dice of the
+    nearest-warped source labels per variant, from the reference itself."""
+    n, h = 32, (1.0, 1.0, 1.0)
+    dims = (n, n, n)
+    out = {}
+    x = np.stack(np.meshgrid(*[np.arange(k) * 1.0 for k in dims], indexing="ij"))
+    for seed in (1, 2):
+        s, t, sl, tl = (a.astype(np.float32) for a in ref.two_disc_case(dims, h, seed))
+        out[f"s{seed}_inputs"] = np.stack([s, t, sl, tl])
+        s, t, sl, tl = (a.astype(np.float64) for a in (s, t, sl, tl))
+        out[f"s{seed}_initial"] = ref.evaluate(dims, h, warped_labels=sl, target_labels=tl)["dice_mean"]
+        for v in ("original", "state_equation", "deformation_state_equation"):
+            m = ref.RefModel(s, t, dims, h, (16, 16, 16), v, 5, 0.05)
+            r = m.optimize(None, max_iter=30, grad_tol=1e-3)
+            fwd, _, _ = m.maps(r["v"])
+            wl = ref.warp(sl, x - fwd, dims, h, "nearest")[0]
+            out[f"s{seed}_{v}_dice"] = ref.evaluate(dims, h, warped_labels=wl, target_labels=tl)["dice_mean"]
+            out[f"s{seed}_{v}_iterations"] = r["iterations"]
+            out[f"s{seed}_{v}_stop"] = ref.STOP_REASONS.index(r["stop"])
+    np.savez_compressed(os.path.join(HERE, "gate8.npz"), **out)
+
+
 if __name__ == "__main__":
     if not ref.available():
         sys.exit("build oracle/_ref first: make -C oracle ref")
@@ -224,6 +248,7 @@ if __name__ == "__main__":
     evaluation()
     cli_register()
     model_rk4()
+    gate8()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
