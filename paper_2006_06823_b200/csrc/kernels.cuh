@@ -54,6 +54,8 @@ struct DftPlan {
   float2* wy_p = nullptr;  // [Ky][Ny]
   // TF32 big/small splits of the z tables for the tensor-core (3xTF32) z stages
   float *tz_e_big = nullptr, *tz_e_small = nullptr, *tz_p_big = nullptr, *tz_p_small = nullptr;
+  // Tz_e big/small in the canonical K-major UMMA layout (tcgen05 embed-z), or null
+  float *uz_e_big = nullptr, *uz_e_small = nullptr;
   long long npts() const { return (long long)N[0] * N[1] * N[2]; }
   long long half() const { return (long long)K[0] * K[1] * (K[2] / 2); }
   long long kprod() const { return (long long)K[0] * K[1] * K[2]; }
@@ -71,6 +73,12 @@ void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int l
 void launch_tc3_gemm(const float* A, int lda, long long sA, const float* Bbig, const float* Bsmall, int ldb, float* C,
                      int ldc, long long sC, int M, int N, int K, int batch, cudaStream_t s);
 void launch_tf32_split(const float* in, float* big, float* small, long long n, cudaStream_t s);
+// tcgen05 3xTF32 embed-z GEMM (umma_gemm.cu): C[b] = A[b] * B, A [M][K] rows, C [M][N] rows
+int umma_padded_n(int N);
+bool umma_zembed_fits(int N, int K);
+void launch_umma_canon_b(const float* Bbig, const float* Bsm, int K, int N, float* Cbig, float* Csm, cudaStream_t s);
+void launch_umma_zembed(const float* A, long long sA, const float* Bbig_c, const float* Bsm_c, float* C, long long sC,
+                        int M, int N, int K, int nb, cudaStream_t s);
 
 // ---- interpolation / transport -------------------------------------------------
 

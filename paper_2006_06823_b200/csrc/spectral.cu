@@ -387,6 +387,16 @@ static bool use_tensor_cores() {
   return v != 0;
 }
 
+// z-embed on tcgen05 (umma_gemm.cu) unless LDDMM_UMMA=0
+static bool use_umma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LDDMM_UMMA");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // embed nf half-band fields D[nf][Kx][Ky][H] -> grid fields out[nf][N] (fp32)
 void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2, float* out, cudaStream_t s) {
   const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
@@ -397,7 +407,10 @@ void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2
   launch_cgemm(p.wx_e, Kx, E1, (long long)Kx * Ny * H, Ny * H, E2, (long long)Nx * Ny * H, Ny * H, Nx, Ny * H,
                Kx, nf, s);
   // Z: for each f: out[(Nx Ny) x Nz] = E2 as float[(Nx Ny) x 2H] * Tz_e[2H x Nz]
-  if (use_tensor_cores())
+  if (use_tensor_cores() && use_umma() && p.uz_e_big)
+    launch_umma_zembed(reinterpret_cast<const float*>(E2), (long long)Nx * Ny * 2 * H, p.uz_e_big, p.uz_e_small, out,
+                       (long long)Nx * Ny * Nz, Nx * Ny, Nz, 2 * H, nf, s);
+  else if (use_tensor_cores())
     launch_tc3_gemm(reinterpret_cast<const float*>(E2), 2 * H, (long long)Nx * Ny * 2 * H, p.tz_e_big, p.tz_e_small,
                     Nz, out, Nz, (long long)Nx * Ny * Nz, Nx * Ny, Nz, 2 * H, nf, s);
   else
