@@ -341,6 +341,148 @@ __device__ __forceinline__ void gw_stage(float* dst_base, const float* __restric
   }
 }
 
+// One 4-node z group of output row (i, j): departure displacements, the SL-regime
+// check (else the global-memory path), weights, the 5 x 5 source rows pl[a] + b P
+// (pl[a] = the staged x-plane a of the neighbourhood, offset to the group's first
+// y row and z window; components CVOL apart) and the stores.
+template <int NC, int P, int CVOL, bool SHIFT>
+__device__ __forceinline__ void gw_item(const float* const (&pl)[5], const float* __restrict__ coef,
+                                        const float* __restrict__ disp, float* __restrict__ out, long long N, int c0,
+                                        int i, int j, int g, int Nx, int Ny, int Nz, float3 sc) {
+  const bool vec = (Nz & 3) == 0;
+  const long long rowp0 = ((long long)i * Ny + j) * Nz;
+  // z of nodes (0,1) and (2,3) of the group
+  const int zA = SHIFT ? (g == 0 ? Nz - 2 : 4 * g - 2) : 4 * g;
+  const int zB = SHIFT ? 4 * g : 4 * g + 2;
+  const int npt = SHIFT ? 4 : min(4, Nz - 4 * g);
+  float dx[4], dy[4], dz[4];
+  if (SHIFT) {
+    const float2 ax = *reinterpret_cast<const float2*>(disp + rowp0 + zA);
+    const float2 bx = *reinterpret_cast<const float2*>(disp + rowp0 + zB);
+    const float2 ay = *reinterpret_cast<const float2*>(disp + N + rowp0 + zA);
+    const float2 by = *reinterpret_cast<const float2*>(disp + N + rowp0 + zB);
+    const float2 az = *reinterpret_cast<const float2*>(disp + 2 * N + rowp0 + zA);
+    const float2 bz = *reinterpret_cast<const float2*>(disp + 2 * N + rowp0 + zB);
+    dx[0] = ax.x; dx[1] = ax.y; dx[2] = bx.x; dx[3] = bx.y;
+    dy[0] = ay.x; dy[1] = ay.y; dy[2] = by.x; dy[3] = by.y;
+    dz[0] = az.x; dz[1] = az.y; dz[2] = bz.x; dz[3] = bz.y;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      dx[m] *= sc.x;
+      dy[m] *= sc.y;
+      dz[m] *= sc.z;
+    }
+  } else if (vec) {
+    const long long p0 = rowp0 + 4 * g;
+    const float4 a = *reinterpret_cast<const float4*>(disp + p0);
+    const float4 b = *reinterpret_cast<const float4*>(disp + N + p0);
+    const float4 cc = *reinterpret_cast<const float4*>(disp + 2 * N + p0);
+    dx[0] = a.x; dx[1] = a.y; dx[2] = a.z; dx[3] = a.w;
+    dy[0] = b.x; dy[1] = b.y; dy[2] = b.z; dy[3] = b.w;
+    dz[0] = cc.x; dz[1] = cc.y; dz[2] = cc.z; dz[3] = cc.w;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      dx[m] *= sc.x;
+      dy[m] *= sc.y;
+      dz[m] *= sc.z;
+    }
+  } else {
+    const long long p0 = rowp0 + 4 * g;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const bool in = m < npt;
+      dx[m] = in ? sc.x * __ldg(disp + p0 + m) : 0.f;
+      dy[m] = in ? sc.y * __ldg(disp + N + p0 + m) : 0.f;
+      dz[m] = in ? sc.z * __ldg(disp + 2 * N + p0 + m) : 0.f;
+    }
+  }
+  float fx[4], fy[4], fz[4];
+  bool ok = true;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    fx[m] = floorf(dx[m]);
+    fy[m] = floorf(dy[m]);
+    fz[m] = floorf(dz[m]);
+    ok = ok && fx[m] >= -1.f && fx[m] <= 0.f && fy[m] >= -1.f && fy[m] <= 0.f && fz[m] >= -1.f && fz[m] <= 0.f;
+  }
+  if (!ok) {
+    for (int m = 0; m < npt; ++m) {
+      const int zm = (m < 2 ? zA : zB) + (m & 1);
+      float v[NC];
+      gather_point_global<NC>(coef + c0 * N, disp, i, j, zm, Nx, Ny, Nz, NC, v, sc);
+      for (int c = 0; c < NC; ++c) out[(c0 + c) * N + rowp0 + zm] = v[c];
+    }
+    return;
+  }
+  // weights of node pairs (0,1) and (2,3) packed as float2 for the sm_100 packed
+  // FFMA2 pipe: each __ffma2_rn is two independent, correctly rounded fmaf.
+  float2 wx[2][5], wy[2][5], wz[2][5];
+#pragma unroll
+  for (int hp = 0; hp < 2; ++hp) {
+    float t0[5], t1[5];
+    w5(dx[2 * hp], fx[2 * hp], t0);
+    w5(dx[2 * hp + 1], fx[2 * hp + 1], t1);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) wx[hp][k] = make_float2(t0[k], t1[k]);
+    w5(dy[2 * hp], fy[2 * hp], t0);
+    w5(dy[2 * hp + 1], fy[2 * hp + 1], t1);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) wy[hp][k] = make_float2(t0[k], t1[k]);
+    w5(dz[2 * hp], fz[2 * hp], t0);
+    w5(dz[2 * hp + 1], fz[2 * hp + 1], t1);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) wz[hp][k] = make_float2(t0[k], t1[k]);
+  }
+  float2 acc[NC][2];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+      const float* rowp = pl[a] + b * P;
+      const float2 w01a = __fmul2_rn(wx[0][a], wy[0][b]);
+      const float2 w01b = __fmul2_rn(wx[1][a], wy[1][b]);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const float4 A = *reinterpret_cast<const float4*>(rowp + c * CVOL);
+        const float4 B = *reinterpret_cast<const float4*>(rowp + c * CVOL + 4);
+        const float win[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+        // nodes (0,1): taps win[k], win[k+1]; nodes (2,3): win[k+2], win[k+3]
+        float2 pa = __fmul2_rn(wz[0][0], make_float2(win[0], win[1]));
+        float2 pb = __fmul2_rn(wz[1][0], make_float2(win[2], win[3]));
+#pragma unroll
+        for (int k = 1; k < 5; ++k) {
+          if (k & 1) {
+            pa.x = fmaf(wz[0][k].x, win[k], pa.x);
+            pa.y = fmaf(wz[0][k].y, win[k + 1], pa.y);
+            pb.x = fmaf(wz[1][k].x, win[k + 2], pb.x);
+            pb.y = fmaf(wz[1][k].y, win[k + 3], pb.y);
+          } else {
+            pa = __ffma2_rn(wz[0][k], make_float2(win[k], win[k + 1]), pa);
+            pb = __ffma2_rn(wz[1][k], make_float2(win[k + 2], win[k + 3]), pb);
+          }
+        }
+        acc[c][0] = __ffma2_rn(w01a, pa, acc[c][0]);
+        acc[c][1] = __ffma2_rn(w01b, pb, acc[c][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    float* o = out + (c0 + c) * N + rowp0;
+    if (SHIFT) {
+      *reinterpret_cast<float2*>(o + zA) = acc[c][0];
+      *reinterpret_cast<float2*>(o + zB) = acc[c][1];
+    } else if (vec) {
+      *reinterpret_cast<float4*>(o + 4 * g) = make_float4(acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y);
+    } else {
+      const float v4[4] = {acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y};
+      for (int m = 0; m < npt; ++m) o[4 * g + m] = v4[m];
+    }
+  }
+}
+
 template <int NC, int TX, int TY, int NTH, int P, bool SHIFT>
 __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __restrict__ coef,
                                            const float* __restrict__ disp, float* __restrict__ out, long long N,
@@ -349,144 +491,14 @@ __device__ __forceinline__ void gw_compute(const float* sbuf, const float* __res
   constexpr int cvol = SX * SY * P;
   const int G = (Nz + 3) >> 2;
   const int items = TX * TY * G;
-  const bool vec = (Nz & 3) == 0;
   for (int it = threadIdx.x; it < items; it += NTH) {
     const int r = it / G, g = it - r * G;
     const int rx = r / TY, ry = r - (r / TY) * TY;
     const int i = x0 + rx, j = y0 + ry;
     if (i >= Nx || j >= Ny) continue;
-    const long long rowp0 = ((long long)i * Ny + j) * Nz;
-    // z of nodes (0,1) and (2,3) of the group
-    const int zA = SHIFT ? (g == 0 ? Nz - 2 : 4 * g - 2) : 4 * g;
-    const int zB = SHIFT ? 4 * g : 4 * g + 2;
-    const int npt = SHIFT ? 4 : min(4, Nz - 4 * g);
-    float dx[4], dy[4], dz[4];
-    if (SHIFT) {
-      const float2 ax = *reinterpret_cast<const float2*>(disp + rowp0 + zA);
-      const float2 bx = *reinterpret_cast<const float2*>(disp + rowp0 + zB);
-      const float2 ay = *reinterpret_cast<const float2*>(disp + N + rowp0 + zA);
-      const float2 by = *reinterpret_cast<const float2*>(disp + N + rowp0 + zB);
-      const float2 az = *reinterpret_cast<const float2*>(disp + 2 * N + rowp0 + zA);
-      const float2 bz = *reinterpret_cast<const float2*>(disp + 2 * N + rowp0 + zB);
-      dx[0] = ax.x; dx[1] = ax.y; dx[2] = bx.x; dx[3] = bx.y;
-      dy[0] = ay.x; dy[1] = ay.y; dy[2] = by.x; dy[3] = by.y;
-      dz[0] = az.x; dz[1] = az.y; dz[2] = bz.x; dz[3] = bz.y;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        dx[m] *= sc.x;
-        dy[m] *= sc.y;
-        dz[m] *= sc.z;
-      }
-    } else if (vec) {
-      const long long p0 = rowp0 + 4 * g;
-      const float4 a = *reinterpret_cast<const float4*>(disp + p0);
-      const float4 b = *reinterpret_cast<const float4*>(disp + N + p0);
-      const float4 cc = *reinterpret_cast<const float4*>(disp + 2 * N + p0);
-      dx[0] = a.x; dx[1] = a.y; dx[2] = a.z; dx[3] = a.w;
-      dy[0] = b.x; dy[1] = b.y; dy[2] = b.z; dy[3] = b.w;
-      dz[0] = cc.x; dz[1] = cc.y; dz[2] = cc.z; dz[3] = cc.w;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        dx[m] *= sc.x;
-        dy[m] *= sc.y;
-        dz[m] *= sc.z;
-      }
-    } else {
-      const long long p0 = rowp0 + 4 * g;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const bool in = m < npt;
-        dx[m] = in ? sc.x * __ldg(disp + p0 + m) : 0.f;
-        dy[m] = in ? sc.y * __ldg(disp + N + p0 + m) : 0.f;
-        dz[m] = in ? sc.z * __ldg(disp + 2 * N + p0 + m) : 0.f;
-      }
-    }
-    float fx[4], fy[4], fz[4];
-    bool ok = true;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      fx[m] = floorf(dx[m]);
-      fy[m] = floorf(dy[m]);
-      fz[m] = floorf(dz[m]);
-      ok = ok && fx[m] >= -1.f && fx[m] <= 0.f && fy[m] >= -1.f && fy[m] <= 0.f && fz[m] >= -1.f && fz[m] <= 0.f;
-    }
-    if (!ok) {
-      for (int m = 0; m < npt; ++m) {
-        const int zm = (m < 2 ? zA : zB) + (m & 1);
-        float v[NC];
-        gather_point_global<NC>(coef + c0 * N, disp, i, j, zm, Nx, Ny, Nz, NC, v, sc);
-        for (int c = 0; c < NC; ++c) out[(c0 + c) * N + rowp0 + zm] = v[c];
-      }
-      continue;
-    }
-    // weights of node pairs (0,1) and (2,3) packed as float2 for the sm_100 packed
-    // FFMA2 pipe: each __ffma2_rn is two independent, correctly rounded fmaf.
-    float2 wx[2][5], wy[2][5], wz[2][5];
-#pragma unroll
-    for (int hp = 0; hp < 2; ++hp) {
-      float t0[5], t1[5];
-      w5(dx[2 * hp], fx[2 * hp], t0);
-      w5(dx[2 * hp + 1], fx[2 * hp + 1], t1);
-#pragma unroll
-      for (int k = 0; k < 5; ++k) wx[hp][k] = make_float2(t0[k], t1[k]);
-      w5(dy[2 * hp], fy[2 * hp], t0);
-      w5(dy[2 * hp + 1], fy[2 * hp + 1], t1);
-#pragma unroll
-      for (int k = 0; k < 5; ++k) wy[hp][k] = make_float2(t0[k], t1[k]);
-      w5(dz[2 * hp], fz[2 * hp], t0);
-      w5(dz[2 * hp + 1], fz[2 * hp + 1], t1);
-#pragma unroll
-      for (int k = 0; k < 5; ++k) wz[hp][k] = make_float2(t0[k], t1[k]);
-    }
-    float2 acc[NC][2];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = make_float2(0.f, 0.f);
     const float* base = sbuf + (rx * SY + ry) * P + 4 * g;
-#pragma unroll
-    for (int a = 0; a < 5; ++a) {
-#pragma unroll
-      for (int b = 0; b < 5; ++b) {
-        const float* rowp = base + (a * SY + b) * P;
-        const float2 w01a = __fmul2_rn(wx[0][a], wy[0][b]);
-        const float2 w01b = __fmul2_rn(wx[1][a], wy[1][b]);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const float4 A = *reinterpret_cast<const float4*>(rowp + c * cvol);
-          const float4 B = *reinterpret_cast<const float4*>(rowp + c * cvol + 4);
-          const float win[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
-          // nodes (0,1): taps win[k], win[k+1]; nodes (2,3): win[k+2], win[k+3]
-          float2 pa = __fmul2_rn(wz[0][0], make_float2(win[0], win[1]));
-          float2 pb = __fmul2_rn(wz[1][0], make_float2(win[2], win[3]));
-#pragma unroll
-          for (int k = 1; k < 5; ++k) {
-            if (k & 1) {
-              pa.x = fmaf(wz[0][k].x, win[k], pa.x);
-              pa.y = fmaf(wz[0][k].y, win[k + 1], pa.y);
-              pb.x = fmaf(wz[1][k].x, win[k + 2], pb.x);
-              pb.y = fmaf(wz[1][k].y, win[k + 3], pb.y);
-            } else {
-              pa = __ffma2_rn(wz[0][k], make_float2(win[k], win[k + 1]), pa);
-              pb = __ffma2_rn(wz[1][k], make_float2(win[k + 2], win[k + 3]), pb);
-            }
-          }
-          acc[c][0] = __ffma2_rn(w01a, pa, acc[c][0]);
-          acc[c][1] = __ffma2_rn(w01b, pb, acc[c][1]);
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      float* o = out + (c0 + c) * N + rowp0;
-      if (SHIFT) {
-        *reinterpret_cast<float2*>(o + zA) = acc[c][0];
-        *reinterpret_cast<float2*>(o + zB) = acc[c][1];
-      } else if (vec) {
-        *reinterpret_cast<float4*>(o + 4 * g) = make_float4(acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y);
-      } else {
-        const float v4[4] = {acc[c][0].x, acc[c][0].y, acc[c][1].x, acc[c][1].y};
-        for (int m = 0; m < npt; ++m) o[4 * g + m] = v4[m];
-      }
-    }
+    const float* const pl[5] = {base, base + SY * P, base + 2 * SY * P, base + 3 * SY * P, base + 4 * SY * P};
+    gw_item<NC, P, cvol, SHIFT>(pl, coef, disp, out, N, c0, i, j, g, Nx, Ny, Nz, sc);
   }
 }
 
@@ -517,6 +529,169 @@ __global__ __launch_bounds__(NTH, 1) void gather_win_kernel(const float* __restr
 
 constexpr int GW_TX = 8, GW_TY = 4, GW_NTH = 512;
 constexpr size_t GW_SMEM_MAX = 227 * 1024;
+
+// ---------------------------------------------------------------------------
+// Marching window gather.  A CTA owns TY output y rows and a segment of x rows and
+// walks x: shared memory holds a ring of GM_RING staged x planes, each the
+// (TY+4) periodic y rows x (P-pitched z row) of FG components.  Output row x needs
+// planes x-2 .. x+2; while it is computed, plane x+3 streams in (cp.async) into the
+// slot plane x-3 vacated, so staging overlaps the FMAs instead of alternating with
+// them, and every source plane is staged once per (y tile, x segment) rather than
+// once per 8 x 4 tile (halo amplification (TY+4)/TY instead of 3).  The per-group
+// arithmetic is gw_item, bitwise the same as the tiled kernel.
+constexpr int GM_RING = 6;
+constexpr int GM_NTH = 512;
+
+template <int FG, int P>
+constexpr int gm_tymax() {
+  constexpr int t = (int)(GW_SMEM_MAX / sizeof(float) / (GM_RING * FG * P)) - 2 * GW_H;
+  return t > 16 ? 16 : t;
+}
+
+template <int NTH, bool SHIFT>
+__device__ __forceinline__ void gm_stage_plane(float* dst_slot, int cvol, const float* __restrict__ coef, long long N,
+                                               int c0, int nc, int x, int y0, int TY, int Nx, int Ny, int Nz,
+                                               int P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int SYr = TY + 2 * GW_H;
+  const int zlen = SHIFT ? Nz + 8 : ((Nz + 3) & ~3) + 2 * GW_H;
+  const long long xoff = (long long)wrapi(x, Nx) * Ny;
+  for (int row = warp; row < nc * SYr; row += NTH / 32) {
+    const int c = row / SYr, jy = row - c * SYr;
+    const float* src = coef + (c0 + c) * N + (xoff + wrapi(y0 - GW_H + jy, Ny)) * Nz;
+    float* dst = dst_slot + c * cvol + jy * P;
+    if (SHIFT) {
+      for (int zz = 4 * lane; zz < zlen; zz += 128) {
+        int gz = zz - 4;
+        gz += gz < 0 ? Nz : 0;
+        gz -= gz >= Nz ? Nz : 0;
+        cp_async16_cg(dst + zz, src + gz);
+      }
+    } else {
+      for (int zz = 2 * lane; zz < zlen; zz += 64) {
+        int gz = zz - GW_H;
+        gz += gz < 0 ? Nz : 0;
+        gz -= gz >= Nz ? Nz : 0;
+        cp_async8(dst + zz, src + gz);
+      }
+    }
+  }
+}
+
+template <int NC, int NTH, int P, int CVOL, int SLOT, bool SHIFT>
+__device__ __forceinline__ void gm_row(const float* smw, int xr, const float* __restrict__ coef,
+                                       const float* __restrict__ disp, float* __restrict__ out, long long N, int c0,
+                                       int i, int y0, int TY, int Nx, int Ny, int Nz, float3 sc) {
+  const int G = (Nz + 3) >> 2;
+  const int items = TY * G;
+  int sl[5];
+#pragma unroll
+  for (int a = 0; a < 5; ++a) sl[a] = ((xr + a) % GM_RING) * SLOT;
+  for (int it = threadIdx.x; it < items; it += NTH) {
+    const int ry = it / G, g = it - ry * G;
+    const int j = y0 + ry;
+    if (j >= Ny) continue;
+    const float* base = smw + ry * P + 4 * g;
+    const float* const pl[5] = {base + sl[0], base + sl[1], base + sl[2], base + sl[3], base + sl[4]};
+    gw_item<NC, P, CVOL, SHIFT>(pl, coef, disp, out, N, c0, i, j, g, Nx, Ny, Nz, sc);
+  }
+}
+
+template <int FG, int NTH, int P, bool SHIFT>
+__global__ __launch_bounds__(NTH, 1) void gather_march_kernel(const float* __restrict__ coef, int F,
+                                                              const float* __restrict__ disp, float* __restrict__ out,
+                                                              int Nx, int Ny, int Nz, float3 sc, int TY, int seg) {
+  constexpr int TYM = gm_tymax<FG, P>();
+  constexpr int CVOL = (TYM + 2 * GW_H) * P;
+  constexpr int SLOT = FG * CVOL;
+  extern __shared__ __align__(16) float smw[];
+  const long long N = (long long)Nx * Ny * Nz;
+  const int x0 = blockIdx.x * seg, nx = min(seg, Nx - x0);
+  const int y0 = blockIdx.y * TY;
+  if (nx <= 0) return;
+  for (int c0 = 0; c0 < F; c0 += FG) {
+    const int nc = min(FG, F - c0);
+    __syncthreads();
+    // prologue: planes x0-2 .. x0+2 in slots 0..4
+    for (int q = 0; q < 5; ++q)
+      gm_stage_plane<NTH, SHIFT>(smw + q * SLOT, CVOL, coef, N, c0, nc, x0 - GW_H + q, y0, TY, Nx, Ny, Nz, P);
+    cp_async_commit();
+    cp_async_wait_group<0>();
+    __syncthreads();
+    for (int xr = 0; xr < nx; ++xr) {
+      // plane x0+xr+3 (needed by row xr+1) into the slot of plane x0+xr-3 (last read by row xr-1)
+      if (xr + 1 < nx)
+        gm_stage_plane<NTH, SHIFT>(smw + ((xr + 5) % GM_RING) * SLOT, CVOL, coef, N, c0, nc, x0 + xr + 3, y0, TY,
+                                   Nx, Ny, Nz, P);
+      cp_async_commit();
+      if (FG >= 3 && nc == 3)
+        gm_row<3, NTH, P, CVOL, SLOT, SHIFT>(smw, xr, coef, disp, out, N, c0, x0 + xr, y0, TY, Nx, Ny, Nz, sc);
+      else if (FG >= 2 && nc == 2)
+        gm_row<2, NTH, P, CVOL, SLOT, SHIFT>(smw, xr, coef, disp, out, N, c0, x0 + xr, y0, TY, Nx, Ny, Nz, sc);
+      else
+        gm_row<1, NTH, P, CVOL, SLOT, SHIFT>(smw, xr, coef, disp, out, N, c0, x0 + xr, y0, TY, Nx, Ny, Nz, sc);
+      cp_async_wait_group<0>();
+      __syncthreads();
+    }
+  }
+}
+
+static bool use_march() {
+  static const bool on = [] {
+    const char* e = std::getenv("LDDMM_GATHER_MARCH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int P, bool SHIFT>
+static bool launch_gm_pitch(const float* coef, int ncomp, const float* disp, float* out, const int* N, float3 sc,
+                            cudaStream_t s) {
+  const int need = SHIFT ? N[2] + 8 : ((N[2] + 3) & ~3) + 2 * GW_H;
+  if (need > P) return false;
+  const int G = (N[2] + 3) / 4;
+  if (G > GM_NTH) return false;
+  const int FG = std::min(3, ncomp);
+  const int tym = FG == 3 ? gm_tymax<3, P>() : FG == 2 ? gm_tymax<2, P>() : gm_tymax<1, P>();
+  if (tym < 1) return false;
+  const int TY = std::max(1, std::min(tym, GM_NTH / G));
+  const int tiles_y = ceil_div(N[1], TY);
+  int nseg = std::max(1, kSMs / tiles_y);
+  const int seg = ceil_div(N[0], nseg);
+  nseg = ceil_div(N[0], seg);
+  const size_t smem = (size_t)GM_RING * FG * (tym + 2 * GW_H) * P * sizeof(float);
+  static bool attr_set[64][3] = {};
+  int dev = 0;
+  LDDMM_CUDA(cudaGetDevice(&dev));
+  dim3 grid(nseg, tiles_y, 1);
+  auto go = [&](auto kern, int k) {
+    if (!attr_set[dev & 63][k]) {
+      LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GW_SMEM_MAX));
+      attr_set[dev & 63][k] = true;
+    }
+    kern<<<grid, GM_NTH, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], sc, TY, seg);
+  };
+  if (FG == 3)
+    go(gather_march_kernel<3, GM_NTH, P, SHIFT>, 2);
+  else if (FG == 2)
+    go(gather_march_kernel<2, GM_NTH, P, SHIFT>, 1);
+  else
+    go(gather_march_kernel<1, GM_NTH, P, SHIFT>, 0);
+  LDDMM_LAUNCH_CHECK();
+  return true;
+}
+
+template <bool SHIFT>
+static bool launch_gm_any(const float* coef, int ncomp, const float* disp, float* out, const int* N, float3 sc,
+                          cudaStream_t s) {
+  return launch_gm_pitch<64, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gm_pitch<128, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gm_pitch<192, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gm_pitch<264, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gm_pitch<392, SHIFT>(coef, ncomp, disp, out, N, sc, s) ||
+         launch_gm_pitch<520, SHIFT>(coef, ncomp, disp, out, N, sc, s);
+}
+
 
 template <int P, bool SHIFT>
 static bool launch_gw_pitch(const float* coef, int ncomp, const float* disp, float* out, const int* N, float3 sc,
@@ -567,10 +742,16 @@ void launch_gather_cubic(const float* coef, int ncomp, const float* disp, float*
 
 // Row pitch: the smallest compiled pitch holding the staged row (Nz + 8 with the
 // shifted groups when Nz % 4 == 0, else Nz + 4 rounded to 4); longer z rows go to
-// the tiled kernel (unit scale only).
+// the tiled kernel (unit scale only).  `march`: the SL-step gathers (sub-voxel
+// departures) take the marching kernel; pull-backs through whole deformation maps
+// (many nodes outside the window regime, served by the global-memory path) keep the
+// tiled kernel, whose 16 waves of small CTAs balance those slow nodes.
 void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
-                          const int* N, cudaStream_t s) {
+                          const int* N, cudaStream_t s, bool march) {
   const float3 sc = make_float3(sx, sy, sz);
+  if (march && use_march() && (N[2] % 4 == 0 ? launch_gm_any<true>(coef, ncomp, disp, out, N, sc, s)
+                                    : launch_gm_any<false>(coef, ncomp, disp, out, N, sc, s)))
+    return;
   if (N[2] % 4 == 0 ? launch_gw_any<true>(coef, ncomp, disp, out, N, sc, s)
                     : launch_gw_any<false>(coef, ncomp, disp, out, N, sc, s))
     return;
@@ -695,7 +876,7 @@ void launch_departure(const float* vgrid, const float* vcoef, double dt, const d
 void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp_phys, const double* h,
                                  float* out, const int* N, cudaStream_t s) {
   launch_gather_scaled(coef, ncomp, disp_phys, -(float)(1.0 / h[0]), -(float)(1.0 / h[1]), -(float)(1.0 / h[2]),
-                       out, N, s);
+                       out, N, s, false);
 }
 
 // ---------------------------------------------------------------------------

@@ -99,7 +99,7 @@ void launch_departure_dir(const float* vgrid, const float* vcoef, double dt, con
                           float* vm, const int* N, cudaStream_t s);
 // gather with the displacement scaled per axis: samples coef at node + (sx dx, sy dy, sz dz)
 void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
-                          const int* N, cudaStream_t s);
+                          const int* N, cudaStream_t s, bool march = true);
 // cubic pull-back of coef at x - disp_phys where disp is a grid field in physical units
 // (points_from_displacement, variants.hpp:49-51); out[c] for ncomp coefficient fields
 void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp_phys, const double* h,
