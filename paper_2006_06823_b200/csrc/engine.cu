@@ -209,6 +209,12 @@ void Engine::build_plan(DftPlan& p, const int* Ng, const int* K, const double* w
   p.tz_p_small = alloc(tz_p.size());
   launch_tf32_split(p.tz_e, p.tz_e_big, p.tz_e_small, (long long)tz_e.size(), stream_);
   launch_tf32_split(p.tz_p, p.tz_p_big, p.tz_p_small, (long long)tz_p.size(), stream_);
+  if (umma_zproject_fits(Nz, 2 * H)) {
+    const size_t nc = (size_t)2 * H * umma_zproject_kpad(Nz);
+    p.uz_p_big = alloc(nc);
+    p.uz_p_small = alloc(nc);
+    launch_umma_zproj_prep(p.tz_p_big, p.tz_p_small, Nz, 2 * H, p.uz_p_big, p.uz_p_small, stream_);
+  }
   if (umma_zembed_fits(Nz, 2 * H)) {
     const size_t nc = (size_t)umma_padded_n(Nz) * 2 * H;
     p.uz_e_big = alloc(nc);

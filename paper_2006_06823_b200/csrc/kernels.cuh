@@ -56,6 +56,8 @@ struct DftPlan {
   float *tz_e_big = nullptr, *tz_e_small = nullptr, *tz_p_big = nullptr, *tz_p_small = nullptr;
   // Tz_e big/small in the canonical K-major UMMA layout (tcgen05 embed-z), or null
   float *uz_e_big = nullptr, *uz_e_small = nullptr;
+  // Tz_p in the canonical UMMA layout, K zero-padded to whole chunks (tcgen05 z-project), or null
+  float *uz_p_big = nullptr, *uz_p_small = nullptr;
   long long npts() const { return (long long)N[0] * N[1] * N[2]; }
   long long half() const { return (long long)K[0] * K[1] * (K[2] / 2); }
   long long kprod() const { return (long long)K[0] * K[1] * K[2]; }
@@ -77,6 +79,13 @@ void launch_tf32_split(const float* in, float* big, float* small, long long n, c
 int umma_padded_n(int N);
 bool umma_zembed_fits(int N, int K);
 void launch_umma_canon_b(const float* Bbig, const float* Bsm, int K, int N, float* Cbig, float* Csm, cudaStream_t s);
+// tcgen05 3xTF32 z-project GEMM (A streamed by cp.async into the canonical layout)
+bool umma_zproject_fits(int K, int N);
+int umma_zproject_kpad(int K);
+void launch_umma_zproj_prep(const float* Bbig, const float* Bsm, int K, int N, float* Cbig, float* Csm,
+                            cudaStream_t s);
+void launch_umma_zproject(const float* A, const float* Bbig_c, const float* Bsm_c, float* C, int M, int K, int N,
+                          cudaStream_t s);
 void launch_umma_zembed(const float* A, long long sA, const float* Bbig_c, const float* Bsm_c, float* C, long long sC,
                         int M, int N, int K, int nb, cudaStream_t s);
 

@@ -17,7 +17,11 @@
 //      (cp.async.bulk, TMA engine) that overlaps the following tile.
 // The output write (4 N bytes per row) dominates the traffic; the kernel runs at
 // ~70% of the measured HBM bandwidth where the mma.sync version ran at ~37%.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <string>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -46,6 +50,18 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// K-major SWIZZLE_128B descriptor (8-row x 128-byte atoms, 1024-byte aligned; the
+// start address moves by 32 bytes per 8-element TF32 K step inside the atom row)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;    // SBO: 8-row atom stride
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+  return d;
+}
+
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
@@ -61,6 +77,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       " @!p bra UMMA_MBAR_WAIT;\n}\n" ::"r"(su32(bar)),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ void cp_async16_zp(float* smem, const float* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(smem)), "l"(gmem) : "memory");
 }
 
 // canonical K-major offset (floats) of element (row, k) in a tile with K columns
@@ -226,6 +246,266 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+// project-z:  C[m][n] = sum_k A[m][k] * B[k][n],  A = nf grid fields viewed as one
+// float [nf*Nx*Ny][Nz] (K = Nz; fields are contiguous), B = Tz_p [Nz][2H] (N = 2H),
+// C = G1 [nf*Nx*Ny][2H].
+//
+// The streaming operand is A (the grid).  One TMA tensor copy per 128-row x ZP_KC
+// (= 128-byte) chunk brings it from HBM straight into the K-major SWIZZLE_128B layout
+// the UMMA descriptor reads (8-row x 128-byte atoms); the K tail and the last
+// tile's missing rows are zero-filled by the TMA unit.  A ZP_NBUF-deep
+// ring keeps ZP_NBUF - 1 chunks in flight while the current one is split in place
+// into TF32 big (mantissa-masked, exact in TF32) + small (a - big, exact in fp32) and
+// fed to 3 x ZP_KC/8 tcgen05.mma.  B (big + small, canonical, K zero-padded to whole
+// chunks) stays in shared memory.  Two TMEM accumulators alternate between 128-row
+// tiles; a tile's epilogue (tcgen05.ld, 16-byte stores of its rows) runs while the
+// next tile's chunks stream in.
+constexpr int ZP_KC = 32;
+constexpr int ZP_NBUF = 6;  // TMA ring depth
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+constexpr int ZP_THREADS = 512;  // warp 0 TMA, warp 1 MMA, warps 4-7 epilogue, warps 8-15 split
+constexpr int ZP_NS = 4;         // small-part buffers
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+
+template <int NT>
+__global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                      const float* __restrict__ Bbig_c,
+                                                                      const float* __restrict__ Bsm_c,
+                                                                      float* __restrict__ C, int M, int Kpad) {
+  constexpr int CH = 128 * ZP_KC;  // floats per chunk buffer
+  constexpr uint32_t LBO_B = 128;
+  constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
+  const uint32_t SBO_B = (uint32_t)(Kpad / 4) * 128;
+  extern __shared__ __align__(1024) float sm[];
+  float* ring = sm;                     // ZP_NBUF chunks: TMA destination, split in place to big
+  float* smallb = ring + ZP_NBUF * CH;  // ZP_NS small chunks
+  float* Bb = smallb + ZP_NS * CH;
+  float* Bs = Bb + NT * Kpad;
+  __shared__ __align__(8) unsigned long long full[ZP_NBUF], split_done[ZP_NBUF], mma_done[ZP_NBUF];
+  __shared__ __align__(8) unsigned long long acc_full[2], acc_free[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(&tmem_base_sh)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < ZP_NBUF; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;\n" ::"r"(su32(&split_done[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&mma_done[i])));
+    }
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&acc_full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;\n" ::"r"(su32(&acc_free[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int e = tid; e < NT * Kpad / 4; e += ZP_THREADS) {
+    reinterpret_cast<float4*>(Bb)[e] = __ldg(reinterpret_cast<const float4*>(Bbig_c) + e);
+    reinterpret_cast<float4*>(Bs)[e] = __ldg(reinterpret_cast<const float4*>(Bsm_c) + e);
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+  const int mtiles = (M + 127) / 128;
+  const int nk = Kpad / ZP_KC;
+  const int my_tiles = (mtiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int S = my_tiles * nk;  // this CTA's chunk sequence
+  auto par = [](int q, int period) { return (uint32_t)(q / period) & 1u; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // TMA producer: chunk q -> ring slot q % ZP_NBUF once chunk q - ZP_NBUF's MMAs are done
+      for (int q = 0; q < S; ++q) {
+        if (q >= ZP_NBUF) mbar_wait(&mma_done[q % ZP_NBUF], par(q - ZP_NBUF, ZP_NBUF));
+        const int tile = (int)blockIdx.x + (q / nk) * (int)gridDim.x, j = q % nk;
+        unsigned long long* bar = &full[q % ZP_NBUF];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
+                     "r"((uint32_t)(CH * 4))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];\n" ::"r"(su32(ring + (q % ZP_NBUF) * CH)),
+            "l"(&tmA), "r"(j * ZP_KC), "r"(tile * 128), "r"(su32(bar))
+            : "memory");
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // MMA issuer
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((128u >> 4) << 24);
+      for (int s = 0; s < S; ++s) {
+        const int t = s / nk, j = s % nk;
+        if (j == 0 && t >= 2) mbar_wait(&acc_free[t & 1], par(t - 2, 2));
+        mbar_wait(&split_done[s % ZP_NBUF], par(s, ZP_NBUF));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)((t & 1) * NT);
+        const uint32_t a_big = su32(ring + (s % ZP_NBUF) * CH), a_sml = su32(smallb + (s % ZP_NS) * CH);
+        const uint32_t b_off = (uint32_t)j * (ZP_KC / 4) * 128;
+        const uint32_t b_big = su32(Bb) + b_off, b_sml = su32(Bs) + b_off;
+        for (int pass = 0; pass < 3; ++pass) {
+          const uint32_t aop = pass == 0 ? a_sml : a_big, bop = pass == 1 ? b_sml : b_big;
+          for (int ks = 0; ks < ZP_KC / 8; ++ks)
+            umma_tf32(acc, umma_desc_sw128(aop + ks * 32), umma_desc(bop + ks * 2 * LBO_B, LBO_B, SBO_B), idesc,
+                      (j | pass | ks) ? 1u : 0u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         su32(&mma_done[s % ZP_NBUF]))
+                     : "memory");
+        if (j == nk - 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           su32(&acc_full[t & 1]))
+                       : "memory");
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // epilogue: TMEM lane quarter warp & 3 -> C rows
+    const int qd = warp & 3;
+    for (int t = 0; t < my_tiles; ++t) {
+      mbar_wait(&acc_full[t & 1], par(t, 2));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t acc = tmem + (uint32_t)((t & 1) * NT);
+      const int m = ((int)blockIdx.x + t * (int)gridDim.x) * 128 + qd * 32 + lane;
+      float* crow = C + (long long)m * NT;
+#pragma unroll
+      for (int c0 = 0; c0 < NT; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(acc + ((uint32_t)(qd * 32) << 16) + c0, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (m < M) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(crow + c0 + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                                                    __uint_as_float(r[i + 2]),
+                                                                    __uint_as_float(r[i + 3]));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(&acc_free[t & 1]);
+    }
+  } else if (warp >= 8) {
+    // split workers: chunk s in place -> TF32 big; small -> small buffer s % ZP_NS
+    const int st = tid - 256;
+    for (int s = 0; s < S; ++s) {
+      mbar_wait(&full[s % ZP_NBUF], par(s, ZP_NBUF));
+      if (s >= ZP_NS) mbar_wait(&mma_done[(s - ZP_NS) % ZP_NBUF], par(s - ZP_NS, ZP_NBUF));
+      float* big = ring + (s % ZP_NBUF) * CH;
+      float* sml = smallb + (s % ZP_NS) * CH;
+#pragma unroll
+      for (int u = 0; u < CH / 4 / 256; ++u) {
+        const int e = st + u * 256;
+        const float4 a = reinterpret_cast<const float4*>(big)[e];
+        float4 bg;
+        bg.x = __uint_as_float(__float_as_uint(a.x) & 0xffffe000u);
+        bg.y = __uint_as_float(__float_as_uint(a.y) & 0xffffe000u);
+        bg.z = __uint_as_float(__float_as_uint(a.z) & 0xffffe000u);
+        bg.w = __uint_as_float(__float_as_uint(a.w) & 0xffffe000u);
+        reinterpret_cast<float4*>(big)[e] = bg;
+        reinterpret_cast<float4*>(sml)[e] = make_float4(a.x - bg.x, a.y - bg.y, a.z - bg.z, a.w - bg.w);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(&split_done[s % ZP_NBUF]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+// Tz_p big/small [K][N] row-major -> canonical K-major [N][Kpad], rows k >= K zero
+__global__ void umma_zproj_prep_kernel(const float* __restrict__ Bbig, const float* __restrict__ Bsm, int K, int N,
+                                       int Kpad, float* __restrict__ Cbig, float* __restrict__ Csm) {
+  const long long total = (long long)N * Kpad;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(e / Kpad), k = (int)(e - (long long)n * Kpad);
+    const bool in = k < K;
+    Cbig[canon_off(n, k, Kpad)] = in ? Bbig[(long long)k * N + n] : 0.f;
+    Csm[canon_off(n, k, Kpad)] = in ? Bsm[(long long)k * N + n] : 0.f;
+  }
+}
+
+int umma_zproject_kpad(int K) { return (K + ZP_KC - 1) / ZP_KC * ZP_KC; }
+
+static size_t umma_zproject_smem(int N, int K) {
+  return ((size_t)2 * N * umma_zproject_kpad(K) + (size_t)(ZP_NBUF + ZP_NS) * 128 * ZP_KC) * sizeof(float);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+bool umma_zproject_fits(int K, int N) {
+  // K = Nz (rows 16-byte aligned, whole 16-byte chunks), N = 2H in {32, 64}
+  return K % 4 == 0 && (N == 32 || N == 64) && umma_zproject_smem(N, K) <= 226 * 1024 &&
+         tensor_map_encoder() != nullptr;
+}
+
+void launch_umma_zproj_prep(const float* Bbig, const float* Bsm, int K, int N, float* Cbig, float* Csm,
+                            cudaStream_t s) {
+  const int Kpad = umma_zproject_kpad(K);
+  umma_zproj_prep_kernel<<<grid_for((long long)N * Kpad, 256), 256, 0, s>>>(Bbig, Bsm, K, N, Kpad, Cbig, Csm);
+  LDDMM_LAUNCH_CHECK();
+}
+
+// A: M rows of K floats (contiguous), C: M rows of N floats (contiguous)
+void launch_umma_zproject(const float* A, const float* Bbig_c, const float* Bsm_c, float* C, int M, int K, int N,
+                          cudaStream_t s) {
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+  const cuuint32_t box[2] = {ZP_KC, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw EngineError(3, "umma z-project: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  const size_t smem = umma_zproject_smem(N, K);
+  const int mtiles = (M + 127) / 128;
+  const int grid = std::min(kSMs, mtiles);
+  auto go = [&](auto kern, int slot) {
+    static bool set[64][2] = {};
+    int dev = 0;
+    LDDMM_CUDA(cudaGetDevice(&dev));
+    if (!set[dev & 63][slot]) {
+      LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+      set[dev & 63][slot] = true;
+    }
+    kern<<<grid, ZP_THREADS, smem, s>>>(tm, Bbig_c, Bsm_c, C, M, umma_zproject_kpad(K));
+  };
+  if (N == 32)
+    go(umma_zproject_kernel<32>, 0);
+  else
+    go(umma_zproject_kernel<64>, 1);
+  LDDMM_LAUNCH_CHECK();
 }
 
 // B [K][N] (big / small TF32 parts, row-major) -> canonical K-major [NP][K], zero padded
