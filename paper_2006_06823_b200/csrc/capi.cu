@@ -302,11 +302,11 @@ int lddmm_register(lddmm_ctx* ctx, const double* I0, const double* I1, const ldd
   return guard(ctx, [&] {
     Engine& e = *ctx->eng;
     e.set_images_host(I0, I1);
-    DevBuf<double2> v(e.vel_elems());
-    LDDMM_CUDA(cudaMemsetAsync(v.p, 0, e.vel_elems() * sizeof(double2), e.stream()));
-    OptimizeResult r = optimize(e, v.p, to_opts(opt));
+    double2* v = e.register_velocity();
+    LDDMM_CUDA(cudaMemsetAsync(v, 0, e.vel_elems() * sizeof(double2), e.stream()));
+    OptimizeResult r = optimize(e, v, to_opts(opt));
     if (host_v)
-      LDDMM_CUDA(cudaMemcpyAsync(host_v, v.p, e.vel_elems() * sizeof(double2), cudaMemcpyDeviceToHost, e.stream()));
+      LDDMM_CUDA(cudaMemcpyAsync(host_v, v, e.vel_elems() * sizeof(double2), cudaMemcpyDeviceToHost, e.stream()));
     e.sync();
     fill_result(r, hist, cap, res);
   });

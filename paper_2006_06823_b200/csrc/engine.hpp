@@ -218,6 +218,15 @@ class Engine {
   bool dker_ready_ = false;
   void ensure_dker();  // per-axis circulant spectral-derivative kernels (spectral.hpp:326-370)
   DevBuf<float> maps_du_;     // 9 derivative fields for the Jacobian (allocated on first use)
+ public:
+  // velocity of lddmm_register (host-buffer path), allocated on first use and reused
+  double2* register_velocity() {
+    if (!reg_v_.p) reg_v_.alloc(vel_elems());
+    return reg_v_.p;
+  }
+
+ private:
+  DevBuf<double2> reg_v_;
   DevBuf<double2> opt_ws_;    // optimizer workspace: 9 velocities
 
   void build_plan(DftPlan& p, const int* Ngrid, const int* K, const double* parent_wunit);
