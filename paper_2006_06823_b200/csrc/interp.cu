@@ -993,11 +993,79 @@ __global__ void circulant_axis_kernel(const double* __restrict__ in, double* __r
   }
 }
 
+// Register-blocked circulant: each thread produces CR consecutive outputs i0 ..
+// i0+CR-1 of its line, so every loaded input feeds CR accumulators, and the circulant
+// taps are read through a sliding window (CR + 7 shared-memory loads per 8 inputs).
+// Each accumulator still sums j = 0 .. n-1 in order with fma: bitwise the same as
+// circulant_axis_kernel (kept for lines shorter than 8).
+constexpr int CR = 8;
+__global__ void circulant_axis_blocked_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                              const double* __restrict__ D, int n, long long stride,
+                                              long long work) {
+  extern __shared__ double sD[];
+  for (int t = threadIdx.x; t < n; t += blockDim.x) sD[t] = D[t];
+  __syncthreads();
+  const int nb = (n + CR - 1) / CR;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < work;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long inner = q % stride;
+    const long long t = q / stride;
+    const int ib = (int)(t % nb);
+    const long long oh = t / nb;
+    const int i0 = ib * CR;
+    const long long base = oh * n * stride + inner;
+    double acc[CR];
+#pragma unroll
+    for (int r = 0; r < CR; ++r) acc[r] = 0.0;
+    auto dmod = [n](int d) {
+      d %= n;
+      return d < 0 ? d + n : d;
+    };
+    int j0 = 0;
+    for (; j0 + 8 <= n; j0 += 8) {
+      // window m = 0 .. CR+6 holds D[(i0 - j0 - 7 + m) mod n]; tap (r, jj) is m = r - jj + 7
+      double w[CR + 7];
+      int d = dmod(i0 - j0 - 7);
+#pragma unroll
+      for (int m = 0; m < CR + 7; ++m) {
+        w[m] = sD[d];
+        d = d + 1 == n ? 0 : d + 1;
+      }
+      double x[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) x[jj] = in[base + (long long)(j0 + jj) * stride];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int r = 0; r < CR; ++r) acc[r] = fma(w[r - jj + 7], x[jj], acc[r]);
+    }
+    for (; j0 < n; ++j0) {
+      const double x = in[base + (long long)j0 * stride];
+      int d = dmod(i0 - j0);
+#pragma unroll
+      for (int r = 0; r < CR; ++r) {
+        acc[r] = fma(sD[d], x, acc[r]);
+        d = d + 1 == n ? 0 : d + 1;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < CR; ++r)
+      if (i0 + r < n) out[base + (long long)(i0 + r) * stride] = acc[r];
+  }
+}
+
 void launch_circulant_axis_f64(const double* in, double* out, const double* D, int axis, const int* N,
                                cudaStream_t s) {
   long long stride = 1;
   for (int b = axis + 1; b < 3; ++b) stride *= N[b];
   const long long total = (long long)N[0] * N[1] * N[2];
+  if (N[axis] >= 8) {
+    const long long work = total / N[axis] * ((N[axis] + CR - 1) / CR);
+    circulant_axis_blocked_kernel<<<grid_for(work, 256, 8), 256, N[axis] * sizeof(double), s>>>(in, out, D, N[axis],
+                                                                                               stride, work);
+    LDDMM_LAUNCH_CHECK();
+    return;
+  }
   circulant_axis_kernel<<<grid_for(total, 256, 16), 256, N[axis] * sizeof(double), s>>>(in, out, D, N[axis],
                                                                                         stride, total);
   LDDMM_LAUNCH_CHECK();
