@@ -311,7 +311,7 @@ def main():
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": False,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32 grid / f64 band", "data": "synthetic",
                "config": workload(),
-               "roofline": {"kernel": "gather_win_kernel (SL cubic gather)", "bound": "hbm",
+               "roofline": {"kernel": "gather_march_kernel (SL cubic gather)", "bound": "hbm",
                             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                             "frac": achieved / hbm, **ncu_traffic(),
                             "algorithmic_bytes_per_launch": g_bytes / g_n if g_n else 0,

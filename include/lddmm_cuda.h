@@ -190,7 +190,8 @@ int lddmm_op_departure(lddmm_ctx* ctx, const double* dev_v, float* dev_dep_fwd, 
 int lddmm_op_band(lddmm_ctx* ctx, int op, const double* dev_a, const double* dev_b, double* dev_out);
 /* the SL cubic gather alone (ScalarSampler::eval_cubic at departure points, interp.hpp:119-159):
  * dev_coef [ncomp][N] spline coefficients, dev_dep [3][N] grid-unit displacements;
- * impl 0 production (register-window), 1 smem-tiled, 2 global-memory (all bitwise equal) */
+ * impl 0 production (marching window), 1 smem-tiled, 2 global-memory, 3 8x4-tile register window
+ * (the pull-back path); all bitwise equal */
 int lddmm_op_gather(lddmm_ctx* ctx, int impl, const float* dev_coef, int ncomp, const float* dev_dep,
                     float* dev_out);
 /* cubic pull-back of grid scalar fields through x - disp (warp with

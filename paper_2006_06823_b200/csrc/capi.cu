@@ -379,6 +379,8 @@ int lddmm_op_gather(lddmm_ctx* ctx, int impl, const float* coef, int ncomp, cons
     int N[3] = {e.problem().dims[0], e.problem().dims[1], e.problem().dims[2]};
     if (impl == 0)
       launch_gather_cubic(coef, ncomp, dep, out, N, e.stream());
+    else if (impl == 3)
+      launch_gather_scaled(coef, ncomp, dep, 1.f, 1.f, 1.f, out, N, e.stream(), false);
     else if (impl == 1)
       launch_gather_cubic_tiled(coef, ncomp, dep, out, N, e.stream());
     else

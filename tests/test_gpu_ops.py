@@ -115,7 +115,8 @@ def test_truncated_products(cuda, dims, band):
 
 @pytest.mark.parametrize("dims,scale", [((20, 18, 36), 0.6), ((17 * 2, 14, 22), 1.7), ((12, 10, 180), 0.9)])
 def test_gather_implementations_bitwise(cuda, dims, scale):
-    """The production register-window gather, the smem-tiled gather and the plain
+    """The production marching gather (impl 0), the 8x4-tile register-window gather
+    (impl 3, used for pull-backs through whole maps), the smem-tiled gather and the plain
     global-memory gather give bitwise identical results (same taps, same order), including
     nodes outside the |floor(d)| <= 1 regime (fallback path) and Nz not a multiple of 4;
     all match the oracle's cubic sampler (interp.hpp:119-159)."""
@@ -126,11 +127,14 @@ def test_gather_implementations_bitwise(cuda, dims, scale):
     dep = np.clip(dep, -3.5, 3.5)
     tc = cuda.from_numpy(coef).cuda()
     td = cuda.from_numpy(dep).cuda()
-    outs = [ops.gather(tc, td, impl).cpu().numpy() for impl in (0, 1, 2)]
+    outs = [ops.gather(tc, td, impl).cpu().numpy() for impl in (0, 1, 2, 3)]
     assert np.array_equal(outs[0], outs[2])
     assert np.array_equal(outs[1], outs[2])
-    outs3 = [ops.gather(tc[:3], td, impl).cpu().numpy() for impl in (0, 2)]
-    assert np.array_equal(outs3[0], outs3[1])
+    assert np.array_equal(outs[3], outs[2])
+    for nc in (1, 2, 3, 4):
+        outs3 = [ops.gather(tc[:nc], td, impl).cpu().numpy() for impl in (0, 3, 2)]
+        assert np.array_equal(outs3[0], outs3[2])
+        assert np.array_equal(outs3[1], outs3[2])
     x = O.identity_map(g)
     for c in (0, 5):
         want = O.sample_cubic(coef[c].astype(np.float64), x + dep.astype(np.float64), g)
