@@ -422,9 +422,12 @@ void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2
 void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, float2* G3, cudaStream_t s) {
   const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
   const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
+  // small product grid: the FFMA tiled GEMM (9 us) beats the mma.sync one (15 us) at
+  // K = Nz = 46 with its unaligned rows (scalar loads in the tensor-core kernel)
+  const bool small = (long long)Nx * Ny * Nz < (1LL << 20);
   if (use_tensor_cores() && use_umma() && p.uz_p_big)
     launch_umma_zproject(f, p.uz_p_big, p.uz_p_small, reinterpret_cast<float*>(G1), nf * Nx * Ny, Nz, 2 * H, s);
-  else if (use_tensor_cores())
+  else if (use_tensor_cores() && !small)
     launch_tc3_gemm(f, Nz, (long long)Nx * Ny * Nz, p.tz_p_big, p.tz_p_small, 2 * H, reinterpret_cast<float*>(G1),
                     2 * H, (long long)Nx * Ny * 2 * H, Nx * Ny, 2 * H, Nz, nf, s);
   else
