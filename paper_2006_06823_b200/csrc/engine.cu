@@ -336,8 +336,7 @@ double Engine::mse_denominator() { return mse_denom_; }
 // generic pipelines
 
 void Engine::embed_fields(const DftPlan& p, const PrepArgs& a, float* out, float2* D, float2* E1, float2* E2) {
-  launch_band_prep(a, p, D, stream_);
-  dft_embed(p, D, a.nf, E1, E2, out, stream_);
+  dft_embed_prep(p, a, D, E1, E2, out, stream_);
 }
 
 void Engine::project_fields(const DftPlan& p, const float* f, const FinArgs& a, float2* G1, float2* G2,

@@ -30,6 +30,45 @@ namespace lddmm_b200 {
 // ---------------------------------------------------------------------------
 // prep: fp64 band -> fp32 half band with fold and symbol
 
+// element (f, fx, fy, fz) of the fp32 half band D (fold, symbols, scale)
+__device__ __forceinline__ float2 prep_value(const PrepArgs& a, int f, int fx, int fy, int fz, int Kx, int Ky, int Kz,
+                                             int Nx, int Ny, int Nz, double wx, double wy, double wz) {
+  float2 out = make_float2(0.f, 0.f);
+  const PrepField pf = a.f[f];
+  if (fx != Kx / 2 && fy != Ky / 2 && pf.src != nullptr) {
+    const double2* C = pf.src;
+    double2 v = C[((long long)fx * Ky + fy) * Kz + fz];
+    if (fz > 0) {
+      const int mx = (Kx - fx) % Kx, my = (Ky - fy) % Ky, mz = Kz - fz;
+      const double2 w = C[((long long)mx * Ky + my) * Kz + mz];
+      v.x += w.x;
+      v.y -= w.y;
+    }
+    const int kx = fx < Kx / 2 ? fx : fx - Kx;
+    const int ky = fy < Ky / 2 ? fy : fy - Ky;
+    const int kz = fz;
+    double s = pf.scale;
+    if (pf.sym & SYM_PREFILTER) {
+      // 1 / B(k), B(k) = prod_a (4 + 2 cos(2 pi k_a / N_a)) / 6 (exact periodic cubic
+      // B-spline prefilter of interp.hpp:23-63 in Fourier form)
+      const double bx = (4.0 + 2.0 * cospi(2.0 * kx / Nx)) / 6.0;
+      const double by = (4.0 + 2.0 * cospi(2.0 * ky / Ny)) / 6.0;
+      const double bz = (4.0 + 2.0 * cospi(2.0 * kz / Nz)) / 6.0;
+      s /= (bx * by * bz);
+    }
+    const int dax = pf.sym & SYM_DERIV_MASK;
+    if (dax) {
+      // band_derivative: multiply by i*omega_a, omega = 2 pi k / (N_a h_a) (spectral.hpp:77-79,419-427)
+      const double om = dax == 1 ? wx * kx : (dax == 2 ? wy * ky : wz * kz);
+      const double re = -v.y * om, im = v.x * om;
+      v.x = re;
+      v.y = im;
+    }
+    out = make_float2((float)(v.x * s), (float)(v.y * s));
+  }
+  return out;
+}
+
 __global__ void band_prep_kernel(PrepArgs a, int Kx, int Ky, int Kz, int Nx, int Ny, int Nz, double wx,
                                  double wy, double wz, float2* __restrict__ D) {
   const int H = Kz / 2;
@@ -43,40 +82,7 @@ __global__ void band_prep_kernel(PrepArgs a, int Kx, int Ky, int Kz, int Nx, int
     r /= H;
     const int fy = (int)(r % Ky);
     const int fx = (int)(r / Ky);
-    float2 out = make_float2(0.f, 0.f);
-    const PrepField pf = a.f[f];
-    if (fx != Kx / 2 && fy != Ky / 2 && pf.src != nullptr) {
-      const double2* C = pf.src;
-      double2 v = C[((long long)fx * Ky + fy) * Kz + fz];
-      if (fz > 0) {
-        const int mx = (Kx - fx) % Kx, my = (Ky - fy) % Ky, mz = Kz - fz;
-        const double2 w = C[((long long)mx * Ky + my) * Kz + mz];
-        v.x += w.x;
-        v.y -= w.y;
-      }
-      const int kx = fx < Kx / 2 ? fx : fx - Kx;
-      const int ky = fy < Ky / 2 ? fy : fy - Ky;
-      const int kz = fz;
-      double s = pf.scale;
-      if (pf.sym & SYM_PREFILTER) {
-        // 1 / B(k), B(k) = prod_a (4 + 2 cos(2 pi k_a / N_a)) / 6 (exact periodic cubic
-        // B-spline prefilter of interp.hpp:23-63 in Fourier form)
-        const double bx = (4.0 + 2.0 * cospi(2.0 * kx / Nx)) / 6.0;
-        const double by = (4.0 + 2.0 * cospi(2.0 * ky / Ny)) / 6.0;
-        const double bz = (4.0 + 2.0 * cospi(2.0 * kz / Nz)) / 6.0;
-        s /= (bx * by * bz);
-      }
-      const int dax = pf.sym & SYM_DERIV_MASK;
-      if (dax) {
-        // band_derivative: multiply by i*omega_a, omega = 2 pi k / (N_a h_a) (spectral.hpp:77-79,419-427)
-        const double om = dax == 1 ? wx * kx : (dax == 2 ? wy * ky : wz * kz);
-        const double re = -v.y * om, im = v.x * om;
-        v.x = re;
-        v.y = im;
-      }
-      out = make_float2((float)(v.x * s), (float)(v.y * s));
-    }
-    D[t] = out;
+    D[t] = prep_value(a, f, fx, fy, fz, Kx, Ky, Kz, Nx, Ny, Nz, wx, wy, wz);
   }
 }
 
@@ -292,10 +298,20 @@ void launch_band_finalize(const FinArgs& a, const DftPlan& p, const float2* G, c
 // per thread.  (The k-chunked cgemm_kernel spent most of its time in barriers and
 // global-load latency on these shapes.)
 
+struct PrepCtx {
+  PrepArgs a;
+  int Kx, Ky, Kz, Nx, Ny, Nz;
+  double wx, wy, wz;
+};
+
+// PREP: the y-embed with the band prep fused in — B[b] (batch b = (f, fx)) is the
+// half-band slab D[f][fx][.][.], computed from the fp64 band while it is staged
+// (bitwise the values band_prep_kernel would have written).
+template <bool PREP>
 __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restrict__ A, int lda,
                                                          const float2* __restrict__ B, long long sB, int ldb,
                                                          float2* __restrict__ C, long long sC, int ldc, int M, int N,
-                                                         int K, int batch) {
+                                                         int K, int batch, const __grid_constant__ PrepCtx pc) {
   extern __shared__ float2 sm2[];
   const int KP = K + 1;  // padded A row (bank spread across rows)
   float2* As = sm2;
@@ -308,10 +324,18 @@ __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restric
   const int tn = (N + 1) / 2, tiles = ((M + 1) / 2) * tn;
   for (int b = blockIdx.x; b < batch; b += gridDim.x) {
     __syncthreads();
-    const float2* Bb = B + b * sB;
-    for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
-      const int k = e / N, n = e - (e / N) * N;
-      cp_async8_f2(Bs + e, Bb + (long long)k * ldb + n);
+    if (PREP) {
+      const int f = b / pc.Kx, fx = b - f * pc.Kx;
+      for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+        const int k = e / N, n = e - (e / N) * N;
+        Bs[e] = prep_value(pc.a, f, fx, k, n, pc.Kx, pc.Ky, pc.Kz, pc.Nx, pc.Ny, pc.Nz, pc.wx, pc.wy, pc.wz);
+      }
+    } else {
+      const float2* Bb = B + b * sB;
+      for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+        const int k = e / N, n = e - (e / N) * N;
+        cp_async8_f2(Bs + e, Bb + (long long)k * ldb + n);
+      }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
@@ -345,19 +369,32 @@ __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restric
   }
 }
 
+static bool cgemm_smem_fits(int M, int N, int K) {
+  return N <= 64 && ((size_t)M * (K + 1) + (size_t)K * N) * sizeof(float2) <= 200 * 1024;
+}
+
+template <bool PREP>
+static void launch_cgemm_smem(const float2* A, int lda, const float2* B, long long sB, int ldb, float2* C,
+                              long long sC, int ldc, int M, int N, int K, int batch, const PrepCtx& pc,
+                              cudaStream_t s) {
+  const size_t smem = ((size_t)M * (K + 1) + (size_t)K * N) * sizeof(float2);
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  LDDMM_CUDA(cudaGetDevice(&dev));
+  if (!attr_set[dev & 63]) {
+    LDDMM_CUDA(
+        cudaFuncSetAttribute(cgemm_smem_kernel<PREP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set[dev & 63] = true;
+  }
+  cgemm_smem_kernel<PREP><<<batch, 256, smem, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, pc);
+  LDDMM_LAUNCH_CHECK();
+}
+
 void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int ldb, float2* C, long long sC,
                   int ldc, int M, int N, int K, int batch, cudaStream_t s) {
-  const size_t smem = ((size_t)M * (K + 1) + (size_t)K * N) * sizeof(float2);
-  if (N <= 64 && smem <= 200 * 1024) {
-    static bool attr_set[64] = {false};
-    int dev = 0;
-    LDDMM_CUDA(cudaGetDevice(&dev));
-    if (!attr_set[dev & 63]) {
-      LDDMM_CUDA(cudaFuncSetAttribute(cgemm_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr_set[dev & 63] = true;
-    }
-    cgemm_smem_kernel<<<batch, 256, smem, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch);
-    LDDMM_LAUNCH_CHECK();
+  if (cgemm_smem_fits(M, N, K)) {
+    static const PrepCtx none{};
+    launch_cgemm_smem<false>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, none, s);
     return;
   }
   dim3 grid(ceil_div(N, CG_BN), ceil_div(M, CG_BM), batch);
@@ -397,12 +434,39 @@ static bool use_umma() {
   return v != 0;
 }
 
+static void dft_embed_xz(const DftPlan& p, int nf, const float2* E1, float2* E2, float* out, cudaStream_t s);
+
 // embed nf half-band fields D[nf][Kx][Ky][H] -> grid fields out[nf][N] (fp32)
 void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2, float* out, cudaStream_t s) {
   const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
-  const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
+  const int Ny = p.N[1];
   // Y: for each (f,kx): E1[Ny x H] = Wy[Ny x Ky] * D[Ky x H]
   launch_cgemm(p.wy_e, Ky, D, (long long)Ky * H, H, E1, (long long)Ny * H, H, Ny, H, Ky, nf * Kx, s);
+  dft_embed_xz(p, nf, E1, E2, out, s);
+}
+
+// band prep + embed with the prep fused into the y stage (no D round trip, one launch
+// fewer); D is only used when the y-stage operands exceed the shared-memory kernel
+void dft_embed_prep(const DftPlan& p, const PrepArgs& a, float2* D, float2* E1, float2* E2, float* out,
+                    cudaStream_t s) {
+  const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
+  const int Ny = p.N[1];
+  if (!cgemm_smem_fits(Ny, H, Ky) || std::getenv("LDDMM_NO_PREP_FUSION")) {
+    launch_band_prep(a, p, D, s);
+    dft_embed(p, D, a.nf, E1, E2, out, s);
+    return;
+  }
+  PrepCtx pc;
+  pc.a = a;
+  pc.Kx = Kx, pc.Ky = Ky, pc.Kz = p.K[2], pc.Nx = p.N[0], pc.Ny = p.N[1], pc.Nz = p.N[2];
+  pc.wx = p.omega_unit[0], pc.wy = p.omega_unit[1], pc.wz = p.omega_unit[2];
+  launch_cgemm_smem<true>(p.wy_e, Ky, nullptr, 0, H, E1, (long long)Ny * H, H, Ny, H, Ky, a.nf * Kx, pc, s);
+  dft_embed_xz(p, a.nf, E1, E2, out, s);
+}
+
+static void dft_embed_xz(const DftPlan& p, int nf, const float2* E1, float2* E2, float* out, cudaStream_t s) {
+  const int Kx = p.K[0], H = p.K[2] / 2;
+  const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
   // X: for each f: E2[Nx x (Ny H)] = Wx[Nx x Kx] * E1[Kx x (Ny H)]
   launch_cgemm(p.wx_e, Kx, E1, (long long)Kx * Ny * H, Ny * H, E2, (long long)Nx * Ny * H, Ny * H, Nx, Ny * H,
                Kx, nf, s);
