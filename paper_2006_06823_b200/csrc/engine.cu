@@ -341,8 +341,7 @@ void Engine::embed_fields(const DftPlan& p, const PrepArgs& a, float* out, float
 
 void Engine::project_fields(const DftPlan& p, const float* f, const FinArgs& a, float2* G1, float2* G2,
                             float2* G3) {
-  dft_project(p, f, a.nf, G1, G2, G3, stream_);
-  launch_band_finalize(a, p, G3, stream_);
+  dft_project_fin(p, f, a, G1, G2, G3, stream_);
 }
 
 // out_i = pi(gather(spline(iota(in_i)), dep)) combined per FinField (advect_state, transport.hpp:67-73)

@@ -68,6 +68,8 @@ void launch_band_finalize(const FinArgs& a, const DftPlan& p, const float2* G, c
 void dft_embed_prep(const DftPlan& p, const PrepArgs& a, float2* D, float2* E1, float2* E2, float* out,
                     cudaStream_t s);
 void dft_embed(const DftPlan& p, const float2* D, int nf, float2* E1, float2* E2, float* out, cudaStream_t s);
+void dft_project_fin(const DftPlan& p, const float* f, const FinArgs& a, float2* G1, float2* G2, float2* G3,
+                     cudaStream_t s);
 void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, float2* G3, cudaStream_t s);
 void launch_sgemm(const float* A, int lda, long long sA, const float* B, int ldb, float* C, int ldc,
                   long long sC, int M, int N, int K, int batch, cudaStream_t s);

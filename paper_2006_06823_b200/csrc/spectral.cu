@@ -304,14 +304,47 @@ struct PrepCtx {
   double wx, wy, wz;
 };
 
-// PREP: the y-embed with the band prep fused in — B[b] (batch b = (f, fx)) is the
-// half-band slab D[f][fx][.][.], computed from the fp64 band while it is staged
-// (bitwise the values band_prep_kernel would have written).
-template <bool PREP>
+struct FinCtx {
+  FinArgs a;
+  int Kx, Ky, Kz;
+};
+
+// one projected half-band value g of output (f, fx, fy, fz) -> the fp64 band field,
+// as band_finalize_kernel computes it (zero Nyquist planes, alpha / beta combine)
+__device__ __forceinline__ void fin_store(const FinCtx& fc, int f, int fx, int fy, int fz, double gx, double gy) {
+  const int H = fc.Kz / 2;
+  if (fx == fc.Kx / 2 || fy == fc.Ky / 2 || fz == H) gx = gy = 0.0;
+  const FinField ff = fc.a.f[f];
+  const long long idx = ((long long)fx * fc.Ky + fy) * fc.Kz + fz;
+  double2 o = make_double2(ff.alpha * gx, ff.alpha * gy);
+  if (ff.add) {
+    const double2 ad = ff.add[idx];
+    o.x += ff.beta * ad.x;
+    o.y += ff.beta * ad.y;
+  }
+  ff.dst[idx] = o;
+}
+
+// y-project output (batch b = (f, fx), row fy, column h < H): its own band entry and
+// the Hermitian mirror entry ((Kx-fx)%Kx, (Ky-fy)%Ky, Kz-h) for 0 < h < H — every
+// band entry of the field is written by exactly one CTA
+__device__ __forceinline__ void fin_pair(const FinCtx& fc, int f, int fx, int fy, int h, float2 g) {
+  fin_store(fc, f, fx, fy, h, g.x, g.y);
+  if (h > 0) fin_store(fc, f, (fc.Kx - fx) % fc.Kx, (fc.Ky - fy) % fc.Ky, fc.Kz - h, g.x, -(double)g.y);
+}
+
+// MODE 1 (PREP): the y-embed with the band prep fused in — B[b] (batch b = (f, fx))
+// is the half-band slab D[f][fx][.][.], computed from the fp64 band while it is
+// staged (bitwise the values band_prep_kernel would have written).
+// MODE 2 (FIN): the y-project with the band finalize fused in — the batch's outputs
+// go straight to the fp64 band fields (fin_pair) instead of G3.
+template <int MODE>
 __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restrict__ A, int lda,
                                                          const float2* __restrict__ B, long long sB, int ldb,
                                                          float2* __restrict__ C, long long sC, int ldc, int M, int N,
-                                                         int K, int batch, const __grid_constant__ PrepCtx pc) {
+                                                         int K, int batch, const __grid_constant__ PrepCtx pc,
+                                                         const __grid_constant__ FinCtx fc) {
+  constexpr bool PREP = MODE == 1, FIN = MODE == 2;
   extern __shared__ float2 sm2[];
   const int KP = K + 1;  // padded A row (bank spread across rows)
   float2* As = sm2;
@@ -359,12 +392,27 @@ __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restric
         c11.x = fmaf(a1.x, b1.x, fmaf(-a1.y, b1.y, c11.x));
         c11.y = fmaf(a1.x, b1.y, fmaf(a1.y, b1.x, c11.y));
       }
-      Cb[(long long)m0 * ldc + n0] = c00;
-      if (n0 + 1 < N) Cb[(long long)m0 * ldc + n0 + 1] = c01;
-      if (m0 + 1 < M) {
-        Cb[(long long)(m0 + 1) * ldc + n0] = c10;
-        if (n0 + 1 < N) Cb[(long long)(m0 + 1) * ldc + n0 + 1] = c11;
+      if (FIN) {
+        const int f = b / fc.Kx, fx = b - f * fc.Kx;
+        fin_pair(fc, f, fx, m0, n0, c00);
+        if (n0 + 1 < N) fin_pair(fc, f, fx, m0, n0 + 1, c01);
+        if (m0 + 1 < M) {
+          fin_pair(fc, f, fx, m0 + 1, n0, c10);
+          if (n0 + 1 < N) fin_pair(fc, f, fx, m0 + 1, n0 + 1, c11);
+        }
+      } else {
+        Cb[(long long)m0 * ldc + n0] = c00;
+        if (n0 + 1 < N) Cb[(long long)m0 * ldc + n0 + 1] = c01;
+        if (m0 + 1 < M) {
+          Cb[(long long)(m0 + 1) * ldc + n0] = c10;
+          if (n0 + 1 < N) Cb[(long long)(m0 + 1) * ldc + n0 + 1] = c11;
+        }
       }
+    }
+    if (FIN) {
+      // the kz = Kz/2 plane (zero projection) of this batch's rows
+      const int f = b / fc.Kx, fx = b - f * fc.Kx;
+      for (int fy = threadIdx.x; fy < M; fy += blockDim.x) fin_store(fc, f, fx, fy, fc.Kz / 2, 0.0, 0.0);
     }
   }
 }
@@ -373,20 +421,20 @@ static bool cgemm_smem_fits(int M, int N, int K) {
   return N <= 64 && ((size_t)M * (K + 1) + (size_t)K * N) * sizeof(float2) <= 200 * 1024;
 }
 
-template <bool PREP>
+template <int MODE>
 static void launch_cgemm_smem(const float2* A, int lda, const float2* B, long long sB, int ldb, float2* C,
                               long long sC, int ldc, int M, int N, int K, int batch, const PrepCtx& pc,
-                              cudaStream_t s) {
+                              const FinCtx& fc, cudaStream_t s) {
   const size_t smem = ((size_t)M * (K + 1) + (size_t)K * N) * sizeof(float2);
   static bool attr_set[64] = {false};
   int dev = 0;
   LDDMM_CUDA(cudaGetDevice(&dev));
   if (!attr_set[dev & 63]) {
     LDDMM_CUDA(
-        cudaFuncSetAttribute(cgemm_smem_kernel<PREP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        cudaFuncSetAttribute(cgemm_smem_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set[dev & 63] = true;
   }
-  cgemm_smem_kernel<PREP><<<batch, 256, smem, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, pc);
+  cgemm_smem_kernel<MODE><<<batch, 256, smem, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, pc, fc);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -394,7 +442,8 @@ void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int l
                   int ldc, int M, int N, int K, int batch, cudaStream_t s) {
   if (cgemm_smem_fits(M, N, K)) {
     static const PrepCtx none{};
-    launch_cgemm_smem<false>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, none, s);
+    static const FinCtx nofin{};
+    launch_cgemm_smem<0>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, none, nofin, s);
     return;
   }
   dim3 grid(ceil_div(N, CG_BN), ceil_div(M, CG_BM), batch);
@@ -460,7 +509,8 @@ void dft_embed_prep(const DftPlan& p, const PrepArgs& a, float2* D, float2* E1, 
   pc.a = a;
   pc.Kx = Kx, pc.Ky = Ky, pc.Kz = p.K[2], pc.Nx = p.N[0], pc.Ny = p.N[1], pc.Nz = p.N[2];
   pc.wx = p.omega_unit[0], pc.wy = p.omega_unit[1], pc.wz = p.omega_unit[2];
-  launch_cgemm_smem<true>(p.wy_e, Ky, nullptr, 0, H, E1, (long long)Ny * H, H, Ny, H, Ky, a.nf * Kx, pc, s);
+  static const FinCtx nofin{};
+  launch_cgemm_smem<1>(p.wy_e, Ky, nullptr, 0, H, E1, (long long)Ny * H, H, Ny, H, Ky, a.nf * Kx, pc, nofin, s);
   dft_embed_xz(p, a.nf, E1, E2, out, s);
 }
 
@@ -483,8 +533,8 @@ static void dft_embed_xz(const DftPlan& p, int nf, const float2* E1, float2* E2,
 }
 
 // project nf grid fields f[nf][N] -> half band G3[nf][Kx][Ky][H]
-void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, float2* G3, cudaStream_t s) {
-  const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
+static void dft_project_zx(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, cudaStream_t s) {
+  const int Kx = p.K[0], H = p.K[2] / 2;
   const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
   // small product grid: the FFMA tiled GEMM (9 us) beats the mma.sync one (15 us) at
   // K = Nz = 46 with its unaligned rows (scalar loads in the tensor-core kernel)
@@ -499,7 +549,32 @@ void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G
                  (long long)Nx * Ny * 2 * H, Nx * Ny, 2 * H, Nz, nf, s);
   launch_cgemm(p.wx_p, Nx, G1, (long long)Nx * Ny * H, Ny * H, G2, (long long)Kx * Ny * H, Ny * H, Kx, Ny * H,
                Nx, nf, s);
+}
+
+void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, float2* G3, cudaStream_t s) {
+  const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
+  const int Ny = p.N[1];
+  dft_project_zx(p, f, nf, G1, G2, s);
   launch_cgemm(p.wy_p, Ny, G2, (long long)Ny * H, H, G3, (long long)Ky * H, H, Ky, H, Ny, nf * Kx, s);
+}
+
+// project + band finalize with the finalize fused into the y stage (no G3 round trip,
+// one launch fewer)
+void dft_project_fin(const DftPlan& p, const float* f, const FinArgs& a, float2* G1, float2* G2, float2* G3,
+                     cudaStream_t s) {
+  const int Kx = p.K[0], Ky = p.K[1], H = p.K[2] / 2;
+  const int Ny = p.N[1];
+  if (!cgemm_smem_fits(Ky, H, Ny) || std::getenv("LDDMM_NO_FIN_FUSION")) {
+    dft_project(p, f, a.nf, G1, G2, G3, s);
+    launch_band_finalize(a, p, G3, s);
+    return;
+  }
+  dft_project_zx(p, f, a.nf, G1, G2, s);
+  static const PrepCtx none{};
+  FinCtx fc;
+  fc.a = a;
+  fc.Kx = Kx, fc.Ky = Ky, fc.Kz = p.K[2];
+  launch_cgemm_smem<2>(p.wy_p, Ny, G2, (long long)Ny * H, H, nullptr, 0, H, Ky, H, Ny, a.nf * Kx, none, fc, s);
 }
 
 }  // namespace lddmm_b200
