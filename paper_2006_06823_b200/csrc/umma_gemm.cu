@@ -17,6 +17,10 @@
 //      (cp.async.bulk, TMA engine) that overlaps the following tile.
 // The output write (4 N bytes per row) dominates the traffic; the kernel runs at
 // ~70% of the measured HBM bandwidth where the mma.sync version ran at ~37%.
+//
+// project-z (umma_zproject_kernel, below): the grid is the streaming operand, brought
+// in by TMA tensor copies (SWIZZLE_128B) through a ring, with warp-specialised split /
+// MMA / epilogue roles handing off through mbarriers.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -77,10 +81,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       " @!p bra UMMA_MBAR_WAIT;\n}\n" ::"r"(su32(bar)),
       "r"(parity)
       : "memory");
-}
-
-__device__ __forceinline__ void cp_async16_zp(float* smem, const float* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(smem)), "l"(gmem) : "memory");
 }
 
 // canonical K-major offset (floats) of element (row, k) in a tile with K columns
