@@ -163,6 +163,42 @@ int launch_linf_partial(long long n, const double2* x, double* part, cudaStream_
   LDDMM_LAUNCH_CHECK();
   return g;
 }
+// Non-finite flag in one launch: block maxima into part[0..g), and the last block to
+// finish (counter in part[kReduceBlocks], reset by that block) reduces them into slot —
+// the same max of 0/1 flags as nonfinite_partial + reduce_final.
+__global__ __launch_bounds__(256) void nonfinite_flag_kernel(long long n, const double2* __restrict__ x, double* part,
+                                                             double* slot) {
+  unsigned* counter = reinterpret_cast<unsigned*>(part + kReduceBlocks);
+  __shared__ bool last;
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = x[i];
+    if (!isfinite(a.x) || !isfinite(a.y)) m = 1.0;
+  }
+  m = block_max(m);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = m;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double v = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v = fmax(v, reinterpret_cast<volatile double*>(part)[b]);
+    v = block_max(v);
+    if (threadIdx.x == 0) {
+      *slot = v;
+      *counter = 0u;
+    }
+  }
+}
+
+void launch_nonfinite_flag(long long n, const double2* x, double* part, double* slot, cudaStream_t s) {
+  nonfinite_flag_kernel<<<red_grid(n), 256, 0, s>>>(n, x, part, slot);
+  LDDMM_LAUNCH_CHECK();
+}
+
 int launch_nonfinite_partial(long long n, const double2* x, double* part, cudaStream_t s) {
   const int g = red_grid(n);
   nonfinite_partial_kernel<<<g, 256, 0, s>>>(n, x, part);

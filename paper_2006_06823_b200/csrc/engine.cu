@@ -96,7 +96,8 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   sacc_.alloc(fmax_small_ * Ms);
 
   part_.alloc(kReduceBlocks);
-  part2_.alloc(kReduceBlocks);
+  part2_.alloc(kReduceBlocks + 1);  // + the counter of launch_nonfinite_flag
+  LDDMM_CUDA(cudaMemset(part2_.p, 0, (kReduceBlocks + 1) * sizeof(double)));
   slots_.alloc(16 + 4096);
   LDDMM_CUDA(cudaMallocHost(&host_slots_, (16 + 4096) * sizeof(double)));
 
@@ -540,8 +541,7 @@ void Engine::departure(const double2* v, float* dep_fwd, float* dep_bwd, double*
 // Non-finite check of the node filled at march step s (transport.hpp:225-228,285,293):
 // enqueue one device flag per step, read all flags back once per solve.
 void Engine::enqueue_finite_check(const double2* node, int step) {
-  const int g = launch_nonfinite_partial(vec_elems(), node, part2_.p, stream_);
-  launch_reduce_final(part2_.p, g, 1, slots_.p + 16 + step, stream_);
+  launch_nonfinite_flag(vec_elems(), node, part2_.p, slots_.p + 16 + step, stream_);
 }
 
 void Engine::finish_finite_checks(int nsteps) {

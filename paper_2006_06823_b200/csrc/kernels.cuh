@@ -143,6 +143,9 @@ void launch_band_divergence(const double2* v, double2* out, const int* K, const 
 int launch_inner_partial(long long n, const double2* x, const double2* y, double* part, cudaStream_t s);
 int launch_linf_partial(long long n, const double2* x, double* part, cudaStream_t s);
 int launch_nonfinite_partial(long long n, const double2* x, double* part, cudaStream_t s);
+// 1.0 into *slot when x holds a non-finite value, else 0.0; part needs kReduceBlocks + 1
+// doubles, the last one a zero-initialised counter
+void launch_nonfinite_flag(long long n, const double2* x, double* part, double* slot, cudaStream_t s);
 void launch_reduce_final(const double* part, int nparts, int op /*0 sum 1 max*/, double* slot, cudaStream_t s);
 
 // ---- grid pointwise (fp32 fields, fp64 reductions) --------------------------------

@@ -37,8 +37,7 @@ Lerp lerp_at(double u, int n) {
 }  // namespace
 
 void Engine::enqueue_finite(const double2* p, long long n, int step) {
-  const int g = launch_nonfinite_partial(n, p, part2_.p, stream_);
-  launch_reduce_final(part2_.p, g, 1, slots_.p + 16 + step, stream_);
+  launch_nonfinite_flag(n, p, part2_.p, slots_.p + 16 + step, stream_);
 }
 
 // TimeVaryingVelocity::sample(t) of the provider velocity (core.hpp:303-315)

@@ -104,8 +104,7 @@ void Engine::solve_image_forward(ProviderState& ps, const double2* m0, double2* 
     FinField outs[1] = {FinField{dst, 1.0, nullptr, 0.0}};
     advect_multi(in, 1, depf(ps, s), outs);
     // the finite check reads a vector-sized block; scalars use their own length
-    const int g = launch_nonfinite_partial(S, dst, part2_.p, stream_);
-    launch_reduce_final(part2_.p, g, 1, slots_.p + 16 + s, stream_);
+    launch_nonfinite_flag(S, dst, part2_.p, slots_.p + 16 + s, stream_);
     prev = dst;
   }
   if (last) LDDMM_CUDA(cudaMemcpyAsync(last, prev, S * sizeof(double2), cudaMemcpyDeviceToDevice, stream_));
@@ -138,8 +137,7 @@ void Engine::solve_scalar_continuity_bwd(ProviderState& ps, const double2* q1, d
     small_product(0, qs, divnode(ps, to), ft, -1.0, jf ? divnode(ps, to) : nullptr, 1.0);  // src(q*)
     launch_axpy(S, 0.5 * sdt, ft, A, tmp, stream_);
     launch_axpy(S, 0.5 * sdt, F, tmp, series + to * S, stream_);
-    const int g = launch_nonfinite_partial(S, series + to * S, part2_.p, stream_);
-    launch_reduce_final(part2_.p, g, 1, slots_.p + 16 + s, stream_);
+    launch_nonfinite_flag(S, series + to * S, part2_.p, slots_.p + 16 + s, stream_);
   }
   finish_finite_checks(nt);
 }
@@ -182,8 +180,7 @@ void Engine::solve_incremental_image(ProviderState& ps, const double2* dv, doubl
     const double2* ins[1] = {in};
     FinField outs[1] = {FinField{series + (s + 1) * S, 1.0, src + (s + 1) * S, 0.5 * dt}};
     advect_multi(ins, 1, depf(ps, s), outs);
-    const int g = launch_nonfinite_partial(S, series + (s + 1) * S, part2_.p, stream_);
-    launch_reduce_final(part2_.p, g, 1, slots_.p + 16 + s, stream_);
+    launch_nonfinite_flag(S, series + (s + 1) * S, part2_.p, slots_.p + 16 + s, stream_);
   }
   finish_finite_checks(nt);
 }
