@@ -377,7 +377,10 @@ int lddmm_op_gather(lddmm_ctx* ctx, int impl, const float* coef, int ncomp, cons
   return guard(ctx, [&] {
     Engine& e = *ctx->eng;
     int N[3] = {e.problem().dims[0], e.problem().dims[1], e.problem().dims[2]};
-    if (impl == 0)
+    if (impl == 4) {
+      shape_require(launch_gather_pipe(coef, ncomp, dep, out, N, make_float3(1.f, 1.f, 1.f), e.stream()),
+                    "lddmm_op_gather: impl 4 (pipelined gather) does not support this grid");
+    } else if (impl == 0)
       launch_gather_cubic(coef, ncomp, dep, out, N, e.stream());
     else if (impl == 3)
       launch_gather_scaled(coef, ncomp, dep, 1.f, 1.f, 1.f, out, N, e.stream(), false);

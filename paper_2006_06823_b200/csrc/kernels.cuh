@@ -110,6 +110,10 @@ void launch_departure(const float* vgrid, const float* vcoef, double dt, const d
 // vm: [3][N] scratch (separate arrival / traced nodes for nonstationary velocities)
 void launch_departure_dir(const float* vgrid, const float* vcoef, double dt, const double* h, float sg, float* out,
                           float* vm, const int* N, cudaStream_t s);
+// pipelined marching gather (gather_pipe.cu); false when the shape is not supported
+bool gather_pipe_supported(const int* N);
+bool launch_gather_pipe(const float* coef, int ncomp, const float* disp, float* out, const int* N, float3 sc,
+                        cudaStream_t s);
 // gather with the displacement scaled per axis: samples coef at node + (sx dx, sy dy, sz dz)
 void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float sx, float sy, float sz, float* out,
                           const int* N, cudaStream_t s, bool march = true);

@@ -20,7 +20,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblddmm_cuda.so")
+# LDDMM_LIB: an alternative in-tree build of the same library (tools/lab variant builds)
+LIB_PATH = os.environ.get("LDDMM_LIB") or os.path.join(_HERE, "liblddmm_cuda.so")
 
 _lib = None
 

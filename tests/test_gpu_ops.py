@@ -135,6 +135,9 @@ def test_gather_implementations_bitwise(cuda, dims, scale):
         outs3 = [ops.gather(tc[:nc], td, impl).cpu().numpy() for impl in (0, 3, 2)]
         assert np.array_equal(outs3[0], outs3[2])
         assert np.array_equal(outs3[1], outs3[2])
+    if dims[2] % 4 == 0 and dims[1] % 2 == 0:
+        # the pipelined TMA gather (production for these shapes) forced
+        assert np.array_equal(ops.gather(tc, td, 4).cpu().numpy(), outs[2])
     x = O.identity_map(g)
     for c in (0, 5):
         want = O.sample_cubic(coef[c].astype(np.float64), x + dep.astype(np.float64), g)
@@ -151,3 +154,27 @@ def test_warp_grid(cuda):
     got = ops.warp(cuda.from_numpy(f).cuda(), cuda.from_numpy(disp).cuda()).cpu().numpy()
     want = O.warp(f[0], O.points_from_displacement(disp, g), g, "cubic")
     assert np.max(np.abs(got[0] - want)) < 2e-5 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("dims", [(180, 210, 180), (256, 256, 256)])
+def test_gather_config_shapes_bitwise(cuda, dims):
+    """BASELINE config 2 / config 4 grids: the production SL gather (pipelined TMA kernel)
+    is bitwise the plain global-memory gather for F = 1, 3, 6 on a sub-voxel departure
+    field with a patch of multi-voxel departures (fallback path), including both periodic
+    y-wrap tiles."""
+    from paper_2006_06823_b200 import lddmm as L
+    torch = cuda
+    g = torch.Generator(device="cuda").manual_seed(5)
+    ctx = L.Context(L.BandSpec(L.GridSpec(dims), (8, 8, 8)), nt=3)
+    ops = L.Ops(ctx)
+    x = [torch.arange(n, device="cuda", dtype=torch.float32) for n in dims]
+    X, Y, Z = torch.meshgrid(*x, indexing="ij")
+    dep = torch.stack([0.3 * torch.sin(6.2832 * (2 * X / dims[0] + Y / dims[1]) + a) *
+                       torch.cos(6.2832 * Z / dims[2] * (a + 1)) for a in range(3)]).contiguous()
+    dep[:, 10:14, 20:30, 5:40] *= 8.0  # |d| up to 2.4 voxels: the global-memory fallback
+    coef = torch.randn((6,) + dims, device="cuda", generator=g)
+    for nc in (1, 3, 6):
+        c = coef[:nc].contiguous()
+        want = ops.gather(c, dep, 2)
+        assert torch.equal(ops.gather(c, dep, 0), want)
+        assert torch.equal(ops.gather(c, dep, 4), want)
