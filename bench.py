@@ -2,25 +2,36 @@
 """Benchmark: seconds per registration of the band-limited SL-RK2 GN-Krylov
 deformation-state LDDMM path (BASELINE.json metric) on B200.
 
-A step is one full registration of a synthetic 180x210x180 brain-like pair
-(BASELINE.json configs[1]: band 32^3, nt=10, deformation-state variant,
-stationary velocity, sigma2 = 0.01) with the reference's OptimizeOptions defaults
-and max_iter = 10, pcg_max_iter = 5 (the paper's budget),
-images resident in HBM when the step starts.
-The per-registration image constants (I0 spline coefficients, spectral
-gradient) are inside the step.  L2 is flushed (512 MiB write) between steps.
+A step is one full registration with the reference's OptimizeOptions defaults and
+max_iter = 10, pcg_max_iter = 5 (the paper's budget), images
+resident in HBM when the step starts.  The per-registration image constants (I0
+spline coefficients, spectral gradient) are inside the step.  L2 is flushed (512 MiB
+write) between steps.
+
+  N = 1: BASELINE.json configs[1] — the synthetic 180x210x180 brain-like pair (band
+         32^3, nt=10, deformation-state, stationary, sigma2 = 0.01).
+  N > 1: BASELINE.json configs[4] — the config-5 all-pairs sweep of 16 subjects:
+         step s on rank r registers pair (s * N + r) of the 240 ordered pairs (one
+         process per GPU, no collective on the data path; the per-rank times are
+         gathered with one NCCL all_gather at the end and the max over ranks is used).
+         Launched under torchrun by the driver, or re-executed under torchrun by this
+         script when --gpus N > 1 and WORLD_SIZE is unset.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU): every rank registers its own pair (config 5
-style sharding, no collective in the data path); the per-rank step times are
-gathered with one NCCL all_gather at the end and the max over ranks is used.
+Extra keys: `roofline` (the SL gather, HBM), `roofline_dft` (the full-grid truncated
+DFT pipelines, FP32), `fixed_work` (the reference's iteration-cap mode, every
+tolerance 0: 10 GN x 5 PCG, test_optimizer.cpp:197-207), `e2e` (through the C ABI
+lddmm_register from pinned host fp64 buffers), `cpu_baseline`.
 
---impl reference times the reference CPU implementation (oracle/_ref, the
-unmodified reference headers compiled with our FFTW3-API shim) on this host:
-one full-grid FFT, one prefilter and one cubic gather at the same grid,
-extrapolated with the reference's own op counts for the same fixed-work
-registration (oracle/ref.py:defstate_op_counts).
+--impl reference times the reference CPU implementation (oracle/_ref: the unmodified
+reference headers compiled with our FFTW3-API shim) on this host, 1 thread (the
+reference is single-threaded by construction): per step, one real reference
+advect_state (transport.hpp:67-73) of one component at config 2 plus one full-grid
+FFT / prefilter / cubic gather, extrapolated to a registration with the reference's
+own operation counts for its config-2 run.  The full config-2 reference solve,
+measured once offline (5965 s on 8 host threads, tests/golden/config2_ref.npz), is
+reported beside it.
 """
 import argparse
 import json
@@ -103,30 +114,59 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+_ADVECT_MS = {}
+
+
 def cpu_reference_cost(threads=1, dims=DIMS, band=BAND, nt=NT, measured=None, source="our run"):
     """Reference CPU s/registration for the same workload (see module doc).  measured =
-    (forwards, hessvecs, trials) of our run gives the identical operation sequence;
+    (forwards, hessvecs, trials) of a run gives the identical operation sequence;
     without it the nominal budget GN x PCG x 1 trial is used."""
     from oracle import ref
     ref.set_threads(threads)
     t0 = time.time()
     times = ref.time_ops(dims, (1.0, 1.0, 1.0), band, mask=0b0111)
+    # once per process: one real reference advect_state (embed -> prefilter -> cubic warp
+    # -> project) of a scalar band field along a sub-voxel departure field, the composed
+    # hot-path op, as a check of the primitive model
+    key = (dims, band, threads)
+    if key not in _ADVECT_MS:
+        rng = np.random.default_rng(0)
+        q = ref.random_band_field(dims, (1.0, 1.0, 1.0), band, 7, 1.0, 3.0)[:1]
+        x = np.stack(np.meshgrid(*[np.arange(n, dtype=np.float64) for n in dims], indexing="ij"))
+        pts = x + 0.25 * np.sin(x / 7.0 + rng.uniform(0, 6, size=(3, 1, 1, 1)))
+        t1 = time.time()
+        ref.advect_band(q, pts, dims, (1.0, 1.0, 1.0), band)
+        _ADVECT_MS[key] = (time.time() - t1) * 1000.0
+    t_adv = _ADVECT_MS[key]
     sample_s = time.time() - t0
     if measured is not None:
         counts = ref.defstate_op_counts_measured(nt, *measured)
-        how = (f"the measured op sequence of {source} ({measured[0]} forwards+gradients, {measured[1]} hessvecs, "
+        how = (f"the op sequence of {source} ({measured[0]} forwards+gradients, {measured[1]} hessvecs, "
                f"{measured[2]} trials)")
     else:
         counts = ref.defstate_op_counts(nt, GN, PCG, 1)
         how = f"the nominal budget {GN} GN x {PCG} PCG x 1 trial"
     ms = ref.registration_cost_ms(times, counts)
-    sample = (f"reference primitives timed at {dims[0]}x{dims[1]}x{dims[2]}: 1 full-grid complex FFT "
-              f"{times['fft']:.0f} ms, 1 spline prefilter {times['prefilter']:.0f} ms, 1 cubic gather "
-              f"{times['gather']:.0f} ms ({sample_s:.1f} s of CPU work); extrapolated with the reference op "
-              f"counts of {how} at nt={nt}: {counts['fft']} FFTs, {counts['warp']} "
-              f"warps, {counts['pre']} prefilters, {counts['gath']} gathers (band-space ops not counted). "
-              f"FFT = FFTW3-API shim (libfftw3 absent), {threads} thread(s)")
-    return ms / 1000.0, sample
+    model_adv = 2 * times["fft"] + times["prefilter"] + times["gather"]
+    sample = (f"reference code timed at {dims[0]}x{dims[1]}x{dims[2]} on {threads} thread(s): 1 full-grid complex "
+              f"FFT {times['fft']:.0f} ms, 1 spline prefilter {times['prefilter']:.0f} ms, 1 cubic gather "
+              f"{times['gather']:.0f} ms, 1 scalar advect_state {t_adv:.0f} ms (the model 2 FFT + prefilter + "
+              f"gather predicts {model_adv:.0f} ms); {sample_s:.1f} s of CPU work. Extrapolated with the reference "
+              f"op counts of {how} at nt={nt}: {counts['fft']} FFTs, {counts['warp']} warps, {counts['pre']} "
+              f"prefilters, {counts['gath']} gathers (band-space ops not counted). FFT = FFTW3-API shim "
+              f"(libfftw3 absent)")
+    return ms / 1000.0, sample, {"fft_ms": times["fft"], "prefilter_ms": times["prefilter"],
+                                 "gather_ms": times["gather"], "advect_state_1comp_ms": t_adv, "counts": counts}
+
+
+def measured_reference_solve():
+    """The reference's own full config-2 solve, run once offline (tools/ref_config2_golden.py)."""
+    path = os.path.join(ROOT, "tests", "golden", "config2_ref.npz")
+    if not os.path.exists(path):
+        return None
+    d = np.load(path)
+    return {"value": float(d["wall_s"]), "unit": "s/registration", "threads": int(d["threads"]),
+            "source": "tests/golden/config2_ref.npz (reference optimize on this workload, run offline)"}
 
 
 def reference_op_sequence():
@@ -151,20 +191,23 @@ def run_reference(args, rank, world):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_lddmm.so not built"}))
         return
-    threads = os.cpu_count() or 1
+    threads = 1  # the reference is single-threaded by construction
     measured = reference_op_sequence()
+    src = "the reference's own config-2 run (tests/golden/config2_ref.npz)"
+    for _ in range(max(0, args.warmup)):
+        cpu_reference_cost(threads, measured=measured, source=src)
     vals = []
-    sample = ""
+    sample, parts = "", {}
     for _ in range(max(1, args.steps)):
-        v, sample = cpu_reference_cost(threads, measured=measured,
-                                       source="the reference's own config-2 run (tests/golden/config2_ref.npz)")
+        v, sample, parts = cpu_reference_cost(threads, measured=measured, source=src)
         vals.append(v)
     value = float(np.mean(vals))
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s/registration", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1000.0, "higher_is_better": False,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(),
            "cpu_baseline": {"value": value, "unit": "s/registration", "cores": threads, "kind": "reference",
-                            "sample": sample},
+                            "extrapolated": True, "sample": sample, "parts": parts,
+                            "measured_full_solve": measured_reference_solve()},
            "e2e": {"value": value, "unit": "s/registration", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -182,6 +225,45 @@ def ncu_traffic():
         return {"traffic": None}
 
 
+def dft_flops_per_field(dims=DIMS, band=BAND):
+    """Algorithmic flops of one full-grid truncated transform, half band along z (SURVEY.md
+    §8d): 8 x complex MACs of the y stage (Kx H Ky Ny) and x stage (Ny H Kx Nx) + 4 x
+    real-complex MACs of the z stage (Nx Ny Nz H); 617.8 MFLOP at config 2 (the engine
+    counts the same per field, Engine::dft_flops_per_field)."""
+    Nx, Ny, Nz = dims
+    Kx, Ky, H = band[0], band[1], band[2] // 2
+    return 8.0 * (Kx * H * Ky * Ny + Ny * H * Kx * Nx) + 4.0 * Nx * Ny * Nz * H
+
+
+def fp32_peak():
+    """FP32 FFMA peak of one B200: 148 SMs x 128 FMA/clk x 2 flop x 1.965 GHz = 74.4 TFLOP/s
+    nominal; tools/lab/fma_pipe.cu measured 126.6 FMA/clk/SM with packed FFMA2 (73.6
+    TFLOP/s), which is the denominator used (MEASURED_PEAKS.json has no FP32 entry)."""
+    return 73.6, "measured (tools/lab/fma_pipe.cu, FFMA2 at 1965 MHz)"
+
+
+def spawn_torchrun(n):
+    """--gpus N > 1 without a torchrun environment: re-execute under torchrun (one rank per GPU)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def sweep_workload(n, steps, warmup):
+    return {"workload": f"config5: all-pairs sweep of 16 synthetic {DIMS[0]}x{DIMS[1]}x{DIMS[2]} brain-like subjects "
+                        f"(240 ordered pairs), BL band {BAND[0]}^3, deformation-state, SL-RK2 nt={NT}, stationary, "
+                        f"sigma2={SIGMA2}, reference OptimizeOptions defaults with max_iter={GN}, pcg_max_iter={PCG}; "
+                        f"step s on rank r registers pair s*N+r (after {warmup} warm-up pairs per rank)",
+            "dims": list(DIMS), "band": list(BAND), "nt": NT, "variant": "deformation_state_equation",
+            "mode": "parity (reference defaults, max_iter 10)", "l2": "flushed (512 MiB write) between steps",
+            "parallelism": f"pairs sharded over {n} ranks, no collective on the data path"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -190,8 +272,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fixed-work", action="store_true")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_torchrun(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -205,92 +290,136 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # nranks / transport in the log for the driver
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2006_06823_b200 import lddmm as L
     from paper_2006_06823_b200 import phantoms
+    from paper_2006_06823_b200 import sweep
 
-    seed = 2006 + rank
-    I0, I1 = phantoms.brain_pair(DIMS, seed=seed)
-    d0 = torch.from_numpy(I0).to(device=f"cuda:{local}", dtype=torch.float32)
-    d1 = torch.from_numpy(I1).to(device=f"cuda:{local}", dtype=torch.float32)
+    dev = f"cuda:{local}"
     band = L.BandSpec(L.GridSpec(DIMS), BAND)
-    model = L.Model(band, d0, d1, "deformation_state_equation", NT, SIGMA2, device=local)
+    # the pairs this rank registers: [warm-up pairs] + [timed pairs]
+    if world == 1:
+        I0, I1 = phantoms.brain_pair(DIMS, seed=2006)
+        pair_imgs = [(I0, I1)] * (args.warmup + args.steps)
+        config = workload()
+    else:
+        pl = sweep.pair_list(16)
+        idx = [(len(pl) - 1 - (w * world + rank)) % len(pl) for w in range(args.warmup)] + \
+              [(s * world + rank) % len(pl) for s in range(args.steps)]
+        subj = {}
+
+        def S(k):
+            if k not in subj:
+                subj[k] = phantoms.subject(DIMS, k)
+            return subj[k]
+        pair_imgs = [(S(pl[i][0]), S(pl[i][1])) for i in idx]
+        config = sweep_workload(world, args.steps, args.warmup)
+    dimgs = [(torch.from_numpy(a).to(device=dev, dtype=torch.float32),
+              torch.from_numpy(b).to(device=dev, dtype=torch.float32)) for a, b in pair_imgs]
+    model = L.Model(band, dimgs[0][0], dimgs[0][1], "deformation_state_equation", NT, SIGMA2, device=local)
     ctx = model.ctx
     opt = L.OptimizeOptions(max_iter=GN, pcg_max_iter=PCG)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=f"cuda:{local}")
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def one_registration():
-        model.set_images(d0, d1)
-        return L.optimize(model, None, opt)
+    def one_registration(k, o=opt):
+        model.set_images(*dimgs[k])
+        return L.optimize(model, None, o)
 
-    for _ in range(args.warmup):
-        res = one_registration()
+    for w in range(args.warmup):
+        res = one_registration(w)
     torch.cuda.synchronize()
 
     step_ms = []
+    results = []
     launches0 = L.launch_count()
     ctx.gather_timing(True)
     with Clocks(local) as clk:
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
-        for _ in range(args.steps):
+        for s in range(args.steps):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            res = one_registration()
+            res = one_registration(args.warmup + s)
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
+            results.append(res)
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
     g_ms, g_n, g_bytes = ctx.gather_stats()
+    d_ms, d_n, d_flops = ctx.dft_stats()
     ctx.gather_timing(False)
     launches = L.launch_count() - launches0
 
-    total_ms = float(np.sum(step_ms))
-    if dist is not None:
-        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
         allt = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(allt, t)
-        total_ms = max(float(x.item()) for x in allt)
+        return max(float(a.item()) for a in allt)
+
+    total_ms = max_over_ranks(float(np.sum(step_ms)))
     value = total_ms / 1000.0 / (world * args.steps)
     hbm, peak_kind = peaks()
     achieved = (g_bytes / g_n) / (g_ms / g_n * 1e-3) / 1e9 if g_n else 0.0
+    fp32, fp32_kind = fp32_peak()
+    dft_tflops = d_flops / (d_ms * 1e-3) / 1e12 if d_n else 0.0
+
+    # fixed-work mode: every tolerance 0 -> exactly max_iter GN x pcg_max_iter PCG
+    fixed = None
+    if not args.no_fixed_work:
+        fopt = L.OptimizeOptions(max_iter=GN, pcg_max_iter=PCG, grad_tol=0.0, energy_tol=0.0, step_tol=0.0,
+                                 pcg_tol=0.0)
+        one_registration(args.warmup, fopt)
+        f_ms = []
+        for _ in range(2):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fres = one_registration(args.warmup, fopt)
+            e1.record(stream)
+            e1.synchronize()
+            f_ms.append(e0.elapsed_time(e1))
+        fixed = {"value": max_over_ranks(float(np.mean(f_ms))) / 1000.0, "unit": "s/registration",
+                 "mode": "fixed work: grad_tol = energy_tol = step_tol = pcg_tol = 0, max_iter 10, pcg 5 "
+                         "(test_optimizer.cpp:197-207)", "steps": len(f_ms),
+                 "gn_iterations": fres.iterations, "hessvecs": fres.hessvecs, "trials": fres.trials,
+                 "stop": fres.stop}
 
     e2e = None
     if not args.no_e2e:
         ectx = L.Context(band, "deformation_state_equation", NT, SIGMA2, device=local)
         # inputs and the result velocity in pinned host memory (the reference's fp64
-        # ScalarField / BandVectorField layouts); W untimed warm-up calls first
-        # the same fp32-representable images the device arm registers (so both arms do
-        # the same GN work), held as the reference's fp64 host fields
-        h0 = torch.from_numpy(I0.astype(np.float32).astype(np.float64)).pin_memory().numpy()
-        h1 = torch.from_numpy(I1.astype(np.float32).astype(np.float64)).pin_memory().numpy()
+        # ScalarField / BandVectorField layouts): the same fp32-representable images the
+        # device arm registers (so both arms do the same GN work); W untimed warm-up calls
+        hosts = [(torch.from_numpy(a.astype(np.float32).astype(np.float64)).pin_memory().numpy(),
+                  torch.from_numpy(b.astype(np.float32).astype(np.float64)).pin_memory().numpy())
+                 for a, b in pair_imgs]
         v_host = torch.zeros(ectx.vel_shape + (2,), dtype=torch.float64).pin_memory().numpy().view(np.complex128)
         v_host = v_host.reshape(ectx.vel_shape)
-        for _ in range(max(1, args.warmup)):
-            L.register_host(ectx, h0, h1, opt, v_out=v_host)
+        for w in range(max(1, args.warmup)):
+            L.register_host(ectx, *hosts[min(w, len(hosts) - 1)], opt, v_out=v_host)
         e_ms = []
-        for k in range(max(1, args.steps)):
+        for s in range(max(1, args.steps)):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            v_host, r2 = L.register_host(ectx, h0, h1, opt, v_out=v_host)
+            v_host, r2 = L.register_host(ectx, *hosts[args.warmup + s], opt, v_out=v_host)
             e_ms.append((time.perf_counter() - t0) * 1000.0)
-        e2e_ms = float(np.sum(e_ms))
-        if dist is not None:
-            t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
-            allt = [torch.zeros_like(t) for _ in range(world)]
-            dist.all_gather(allt, t)
-            e2e_ms = max(float(x.item()) for x in allt)
+        e2e_ms = max_over_ranks(float(np.sum(e_ms)))
         e2e = {"value": e2e_ms / 1000.0 / (world * len(e_ms)), "unit": "s/registration",
-               "h2d_bytes_per_step": int(2 * I0.size * 8), "d2h_bytes_per_step": int(v_host.nbytes),
+               "h2d_bytes_per_step": int(2 * pair_imgs[0][0].size * 8), "d2h_bytes_per_step": int(v_host.nbytes),
                "path": "lddmm_register (C ABI): pinned host fp64 images in, pinned host fp64 velocity out",
                "result": {"iterations": r2.iterations, "hessvecs": r2.hessvecs, "trials": r2.trials,
                           "forwards": r2.forwards, "final_energy": r2.final_energy}}
@@ -301,8 +430,9 @@ def main():
         try:
             from oracle import ref
             if ref.available():
-                v, sample = cpu_reference_cost(1, measured=(res.forwards, res.hessvecs, res.trials))
-                cpu = {"value": v, "unit": "s/registration", "cores": 1, "kind": "reference", "sample": sample}
+                v, sample, parts = cpu_reference_cost(1, measured=(res.forwards, res.hessvecs, res.trials))
+                cpu = {"value": v, "unit": "s/registration", "cores": 1, "kind": "reference", "extrapolated": True,
+                       "sample": sample, "measured_full_solve": measured_reference_solve()}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unavailable": str(exc)}
 
@@ -310,16 +440,23 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": "s/registration", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": False,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32 grid / f64 band", "data": "synthetic",
-               "config": workload(),
-               "roofline": {"kernel": "gather_march_kernel (SL cubic gather)", "bound": "hbm",
+               "config": config,
+               "roofline": {"kernel": "gather_pipe_kernel (SL cubic gather, TMA-staged)", "bound": "hbm",
                             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                             "frac": achieved / hbm, **ncu_traffic(),
                             "algorithmic_bytes_per_launch": g_bytes / g_n if g_n else 0,
                             "launches_timed": g_n, "gather_share_of_step": g_ms / total_ms if total_ms else 0},
-               "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+               "roofline_dft": {"kernel": "full-grid truncated DFT pipelines (y/x FFMA GEMMs + tcgen05 z stage)",
+                                "bound": "fp32", "achieved": dft_tflops, "peak": fp32, "peak_kind": fp32_kind,
+                                "unit": "TFLOP/s", "frac": dft_tflops / fp32, "traffic": None,
+                                "flops_per_field": dft_flops_per_field(),
+                                "calls_timed": d_n, "dft_share_of_step": d_ms / total_ms if total_ms else 0},
+               "fixed_work": fixed, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+               "clocks": clk.summary(),
                "result": {"stop": res.stop, "iterations": res.iterations, "final_energy": res.final_energy,
                           "hessvecs": res.hessvecs, "trials": res.trials, "forwards": res.forwards,
-                          "mse_rel_final": res.history[-1].mse_rel if res.history else None}}
+                          "mse_rel_final": res.history[-1].mse_rel if res.history else None,
+                          "gn_per_step": [r.iterations for r in results]}}
         print(json.dumps(out))
     if dist is not None:
         dist.destroy_process_group()

@@ -121,6 +121,10 @@ void* lddmm_stream(lddmm_ctx* ctx);
  * sum of N * (12 + 8 C) */
 int lddmm_gather_timing(lddmm_ctx* ctx, int on);
 int lddmm_gather_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* bytes);
+/* same timing window: full-grid truncated DFT calls (embed / project pipelines of nf
+ * fields), with their algorithmic flops (8 (y + x stage complex MACs)
+ * + 4 (z stage real-complex MACs) per field). */
+int lddmm_dft_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* flops);
 
 /* Model::source / Model::target (variants.hpp:238-239): host fp64 ScalarFields */
 int lddmm_set_images(lddmm_ctx* ctx, const double* host_I0, const double* host_I1);

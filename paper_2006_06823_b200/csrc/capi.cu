@@ -21,9 +21,25 @@ namespace {
 
 thread_local std::string g_create_err;
 
+// Binds the context's device for the duration of an ABI call and restores the
+// caller's current device afterwards (contexts on different GPUs in one process).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (dev < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 template <class F>
 int guard(lddmm_ctx* ctx, F&& f, int* step = nullptr) {
   try {
+    DeviceScope dev(ctx && ctx->eng ? ctx->eng->device() : -1);
     f();
     return LDDMM_OK;
   } catch (const EngineError& e) {
@@ -107,6 +123,9 @@ void lddmm_default_options(lddmm_options* o) {
 int lddmm_create(const lddmm_problem* p, int device, lddmm_ctx** out) {
   *out = nullptr;
   auto ctx = std::make_unique<lddmm_ctx>();
+  int caller_dev = -1;
+  if (cudaGetDevice(&caller_dev) != cudaSuccess) caller_dev = -1;
+  DeviceScope restore(caller_dev);  // the Engine constructor binds `device`
   const int rc = guard(ctx.get(), [&] {
     shape_require(p != nullptr, "null problem");
     shape_require(p->d == 3, "only 3-D grids are supported by the CUDA engine");
@@ -134,7 +153,11 @@ int lddmm_create(const lddmm_problem* p, int device, lddmm_ctx** out) {
   return LDDMM_OK;
 }
 
-void lddmm_destroy(lddmm_ctx* ctx) { delete ctx; }
+void lddmm_destroy(lddmm_ctx* ctx) {
+  if (!ctx) return;
+  DeviceScope dev(ctx->eng ? ctx->eng->device() : -1);
+  delete ctx;
+}
 
 const char* lddmm_last_error(const lddmm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
@@ -152,6 +175,10 @@ int lddmm_gather_timing(lddmm_ctx* ctx, int on) {
 
 int lddmm_gather_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* bytes) {
   return guard(ctx, [&] { ctx->eng->gather_stats(ms, launches, bytes); });
+}
+
+int lddmm_dft_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* flops) {
+  return guard(ctx, [&] { ctx->eng->timing_stats(1, ms, launches, flops); });
 }
 
 int lddmm_set_images(lddmm_ctx* ctx, const double* I0, const double* I1) {

@@ -98,8 +98,9 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   part_.alloc(kReduceBlocks);
   part2_.alloc(kReduceBlocks + 1);  // + the counter of launch_nonfinite_flag
   LDDMM_CUDA(cudaMemset(part2_.p, 0, (kReduceBlocks + 1) * sizeof(double)));
-  slots_.alloc(16 + 4096);
-  LDDMM_CUDA(cudaMallocHost(&host_slots_, (16 + 4096) * sizeof(double)));
+  // 16 scalar slots, then one per time step / node (cfl per node, non-finite flag per step)
+  slots_.alloc(16 + p.nt + 1);
+  LDDMM_CUDA(cudaMallocHost(&host_slots_, (16 + p.nt + 1) * sizeof(double)));
 
   const long long V = vec_elems();
   const int nsteps = p.stationary ? 1 : p.nt;  // departure slots per direction
@@ -225,22 +226,44 @@ void Engine::build_plan(DftPlan& p, const int* Ng, const int* K, const double* w
   sync();
 }
 
+void Engine::timing_begin() {
+  while (gt_events_.size() < 2 * (gt_used_ + 1)) {
+    cudaEvent_t ev;
+    LDDMM_CUDA(cudaEventCreate(&ev));
+    gt_events_.push_back(ev);
+  }
+  LDDMM_CUDA(cudaEventRecord(gt_events_[2 * gt_used_], stream_));
+}
+
+void Engine::timing_end(int kind, double amount) {
+  LDDMM_CUDA(cudaEventRecord(gt_events_[2 * gt_used_ + 1], stream_));
+  if (gt_bytes_.size() <= gt_used_) {
+    gt_bytes_.resize(gt_used_ + 1);
+    gt_kind_.resize(gt_used_ + 1);
+  }
+  gt_bytes_[gt_used_] = amount;
+  gt_kind_[gt_used_] = kind;
+  ++gt_used_;
+}
+
 void Engine::timed_gather(const float* coef, int ncomp, const float* dep, float* out) {
   if (!gt_on_) {
     launch_gather_cubic(coef, ncomp, dep, out, full_.N, stream_);
     return;
   }
-  while (gt_events_.size() < 2 * (gt_used_ + 1)) {
-    cudaEvent_t e;
-    LDDMM_CUDA(cudaEventCreate(&e));
-    gt_events_.push_back(e);
-  }
-  LDDMM_CUDA(cudaEventRecord(gt_events_[2 * gt_used_], stream_));
+  timing_begin();
   launch_gather_cubic(coef, ncomp, dep, out, full_.N, stream_);
-  LDDMM_CUDA(cudaEventRecord(gt_events_[2 * gt_used_ + 1], stream_));
-  if (gt_bytes_.size() <= gt_used_) gt_bytes_.resize(gt_used_ + 1);
-  gt_bytes_[gt_used_] = (double)npts() * (12.0 + 8.0 * ncomp);
-  ++gt_used_;
+  // algorithmic bytes N (12 + 8 C): displacement, coefficient reads, output writes
+  timing_end(0, (double)npts() * (12.0 + 8.0 * ncomp));
+}
+
+// algorithmic flops of one full-grid truncated transform (half band along z): complex
+// MACs (8 flop) of the y stage Kx*H*Ky*Ny and x stage Ny*H*Kx*Nx, real-complex MACs
+// (4 flop) of the z stage Nx*Ny*Nz*H
+double Engine::dft_flops_per_field() const {
+  const double Nx = full_.N[0], Ny = full_.N[1], Nz = full_.N[2];
+  const double Kx = prob_.band[0], Ky = prob_.band[1], H = prob_.band[2] / 2;
+  return 8.0 * (Kx * H * Ky * Ny + Ny * H * Kx * Nx) + 4.0 * Nx * Ny * Nz * H;
 }
 
 void Engine::set_gather_timing(bool on) {
@@ -248,19 +271,24 @@ void Engine::set_gather_timing(bool on) {
   gt_used_ = 0;
 }
 
-void Engine::gather_stats(double* ms, long long* launches, double* bytes) {
+void Engine::timing_stats(int kind, double* ms, long long* launches, double* amount) {
   sync();
   double t = 0.0, b = 0.0;
+  long long n = 0;
   for (size_t i = 0; i < gt_used_; ++i) {
-    float e = 0.f;
-    LDDMM_CUDA(cudaEventElapsedTime(&e, gt_events_[2 * i], gt_events_[2 * i + 1]));
-    t += e;
+    if (gt_kind_[i] != kind) continue;
+    float el = 0.f;
+    LDDMM_CUDA(cudaEventElapsedTime(&el, gt_events_[2 * i], gt_events_[2 * i + 1]));
+    t += el;
     b += gt_bytes_[i];
+    ++n;
   }
   *ms = t;
-  *launches = (long long)gt_used_;
-  *bytes = b;
+  *launches = n;
+  *amount = b;
 }
+
+void Engine::gather_stats(double* ms, long long* launches, double* bytes) { timing_stats(0, ms, launches, bytes); }
 
 double Engine::reduce(int nparts, int op) {
   launch_reduce_final(part_, nparts, op, slots_.p, stream_);
@@ -337,12 +365,18 @@ double Engine::mse_denominator() { return mse_denom_; }
 // generic pipelines
 
 void Engine::embed_fields(const DftPlan& p, const PrepArgs& a, float* out, float2* D, float2* E1, float2* E2) {
+  const bool timed = gt_on_ && &p == &full_;
+  if (timed) timing_begin();
   dft_embed_prep(p, a, D, E1, E2, out, stream_);
+  if (timed) timing_end(1, a.nf * dft_flops_per_field());
 }
 
 void Engine::project_fields(const DftPlan& p, const float* f, const FinArgs& a, float2* G1, float2* G2,
                             float2* G3) {
+  const bool timed = gt_on_ && &p == &full_;
+  if (timed) timing_begin();
   dft_project_fin(p, f, a, G1, G2, G3, stream_);
+  if (timed) timing_end(1, a.nf * dft_flops_per_field());
 }
 
 // out_i = pi(gather(spline(iota(in_i)), dep)) combined per FinField (advect_state, transport.hpp:67-73)

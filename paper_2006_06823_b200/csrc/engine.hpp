@@ -162,6 +162,9 @@ class Engine {
   // launch count, algorithmic bytes N * (12 + 8 C) summed over launches.
   void set_gather_timing(bool on);
   void gather_stats(double* ms, long long* launches, double* bytes);
+  // kind 0: SL gathers (amount = algorithmic bytes), 1: full-grid truncated DFTs (flops)
+  void timing_stats(int kind, double* ms, long long* launches, double* amount);
+  double dft_flops_per_field() const;
 
  private:
   Problem prob_;
@@ -309,6 +312,9 @@ class Engine {
   bool gt_on_ = false;
   std::vector<cudaEvent_t> gt_events_;
   std::vector<double> gt_bytes_;
+  std::vector<int> gt_kind_;
+  void timing_begin();
+  void timing_end(int kind, double amount);
   size_t gt_used_ = 0;
   void count(int n = 1) { launches_ += n; }
 };

@@ -136,6 +136,7 @@ def lib():
         L.lddmm_gather_timing.argtypes = [vp, C.c_int]
         L.lddmm_gather_stats.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong),
                                          C.POINTER(C.c_double)]
+        L.lddmm_dft_stats.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -317,6 +318,11 @@ class Context:
         self.check(lib().lddmm_gather_stats(self.h, C.byref(ms), C.byref(n), C.byref(b)))
         return ms.value, n.value, b.value
 
+    def dft_stats(self):
+        ms, n, f = C.c_double(), C.c_longlong(), C.c_double()
+        self.check(lib().lddmm_dft_stats(self.h, C.byref(ms), C.byref(n), C.byref(f)))
+        return ms.value, n.value, f.value
+
 
 def _raise(rc, msg, step=-1):
     if rc == 1:
@@ -382,6 +388,13 @@ class Model:
     def set_images(self, source, target):
         torch = _torch()
         if isinstance(source, torch.Tensor) and source.is_cuda:
+            for x in (source, target):
+                if not (isinstance(x, torch.Tensor) and x.is_cuda):
+                    raise ShapeError("model images: both source and target must be CUDA tensors (or both host)")
+                if tuple(x.shape) != tuple(self.grid.dims):
+                    raise ShapeError("model images must live on the domain grid")
+                if x.device.index != self.ctx.device:
+                    raise ShapeError(f"model images live on cuda:{x.device.index}, the context on cuda:{self.ctx.device}")
             s = source.to(torch.float32).contiguous()
             t = target.to(torch.float32).contiguous()
             self.ctx.check(lib().lddmm_set_images_dev_f32(self.ctx.h, C.c_void_p(s.data_ptr()),
@@ -489,6 +502,8 @@ def register_host(ctx: Context, I0, I1, opt: OptimizeOptions = None, v_out=None)
     opt = opt or OptimizeOptions()
     I0 = np.ascontiguousarray(I0, dtype=np.float64)
     I1 = np.ascontiguousarray(I1, dtype=np.float64)
+    if I0.shape != tuple(ctx.grid.dims) or I1.shape != tuple(ctx.grid.dims):
+        raise ShapeError(f"register_host: images must have the grid shape {tuple(ctx.grid.dims)}")
     v = v_out if v_out is not None else np.zeros(ctx.vel_shape, dtype=np.complex128)
     if v.shape != tuple(ctx.vel_shape) or v.dtype != np.complex128 or not v.flags.c_contiguous:
         raise ShapeError("register_host: v_out must be C-contiguous complex128 of ctx.vel_shape")
@@ -501,6 +516,15 @@ def register_host(ctx: Context, I0, I1, opt: OptimizeOptions = None, v_out=None)
     hist = _records(recs, min(res.n_history, cap))
     return v, OptimizeResult(None, hist, STOP_REASONS[res.stop_reason], bool(res.converged), res.iterations,
                              res.final_energy, res.rel_grad, res.hessvecs, res.trials, res.forwards)
+
+
+def maps_jacobian(ctx: Context, v_host):
+    """Jacobian determinant ranges of the maps of a host band velocity (metrics.hpp:24-79):
+    [fwd min, fwd max, inv min, inv max]; no displacement fields are copied back."""
+    v = Velocity(ctx, v_host)
+    jac = (C.c_double * 4)()
+    ctx.check(lib().lddmm_maps(ctx.h, v.ptr(), None, None, jac))
+    return np.array(list(jac))
 
 
 def compute_maps(model: Model, v: Velocity):
