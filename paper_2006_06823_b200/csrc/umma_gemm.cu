@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 
 #include "common.cuh"
@@ -92,21 +93,30 @@ __host__ __device__ __forceinline__ int canon_off(int row, int k, int K) {
 
 constexpr int UZ_THREADS = 256;
 
+// nsplit > 1 (large Nz, e.g. config 4's 256 x K = 64, whose whole-row plan needs 320 KB):
+// each CTA owns the output columns [h NS, (h+1) NS), h = blockIdx.x % nsplit, NS = N /
+// nsplit (gridDim.x a multiple of nsplit, so h is fixed per CTA); its B slice is the
+// contiguous canonical rows h NS ..; the 64-row stages (64 x NS) are written with a 3-D
+// TMA tensor store (tmC: [nb][M][N], box {NS, 64, 1}) instead of one 1-D bulk copy.
 template <int TMEM_COLS>
 __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float* __restrict__ A, long long sA,
                                                                     const float* __restrict__ Bbig_c,
                                                                     const float* __restrict__ Bsm_c,
                                                                     float* __restrict__ C, long long sC, int M,
-                                                                    int N, int NP, int K, int nb) {
+                                                                    int N, int NP, int K, int nb, int nsplit,
+                                                                    const __grid_constant__ CUtensorMap tmC) {
   const int KC = K / 4;
   const uint32_t LBO = 128, SBO = (uint32_t)KC * 128;
+  const int half = (int)blockIdx.x % nsplit;
+  const int NS = nsplit > 1 ? N / nsplit : N;   // output columns of this CTA (stage row pitch)
+  const int NPS = nsplit > 1 ? NS : NP;          // MMA N (padded)
   extern __shared__ __align__(1024) float sm[];
   float* Bb = sm;
-  float* Bs = Bb + NP * K;
-  float* Ab = Bs + NP * K;
+  float* Bs = Bb + NPS * K;
+  float* Ab = Bs + NPS * K;
   float* As = Ab + 128 * K;
   float* stage0 = As + 128 * K;  // two 64-row halves, each the half tile's image in C
-  float* stage1 = stage0 + 64 * N;
+  float* stage1 = stage0 + 64 * NS;
   __shared__ __align__(8) unsigned long long mbar;
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -119,21 +129,27 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int e = tid; e < NP * K / 4; e += UZ_THREADS) {
-    reinterpret_cast<float4*>(Bb)[e] = __ldg(reinterpret_cast<const float4*>(Bbig_c) + e);
-    reinterpret_cast<float4*>(Bs)[e] = __ldg(reinterpret_cast<const float4*>(Bsm_c) + e);
+  {
+    // canonical K-major rows n0 .. n0 + NPS - 1 are contiguous (n0 a multiple of 8)
+    const float4* bg = reinterpret_cast<const float4*>(Bbig_c + (size_t)half * NPS * K);
+    const float4* bs = reinterpret_cast<const float4*>(Bsm_c + (size_t)half * NPS * K);
+    for (int e = tid; e < NPS * K / 4; e += UZ_THREADS) {
+      reinterpret_cast<float4*>(Bb)[e] = __ldg(bg + e);
+      reinterpret_cast<float4*>(Bs)[e] = __ldg(bs + e);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
   const int mtiles = (M + 127) / 128;
-  const int ntiles = mtiles * nb;
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((128u >> 4) << 24);
+  const int ntiles = mtiles * nb * nsplit;  // work items: (tile, column slice)
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NPS >> 3) << 17) | ((128u >> 4) << 24);
   constexpr int MAXPER = 128 * 16 / UZ_THREADS;  // K <= 64
   const int per = 128 * KC / UZ_THREADS;
   float4 v[MAXPER];
-  auto load_tile = [&](int tile) {
+  auto load_tile = [&](int item) {
+    const int tile = item / nsplit;
     const int b = tile / mtiles, m0 = (tile - b * mtiles) * 128;
     const float* Ag = A + b * sA;
 #pragma unroll
@@ -142,13 +158,14 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
       const int e = tid + q * UZ_THREADS;
       const int r = e & 127, kc = e >> 7;
       const int gm = m0 + r;
-      v[q] = (tile < ntiles && gm < M) ? __ldg(reinterpret_cast<const float4*>(Ag + (long long)gm * K) + kc)
+      v[q] = (item < ntiles && gm < M) ? __ldg(reinterpret_cast<const float4*>(Ag + (long long)gm * K) + kc)
                                        : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
   uint32_t phase = 0;
   load_tile(blockIdx.x);
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int item = blockIdx.x; item < ntiles; item += gridDim.x) {
+    const int tile = item / nsplit;
     const int b = tile / mtiles, m0 = (tile - b * mtiles) * 128;
 #pragma unroll
     for (int q = 0; q < MAXPER; ++q) {
@@ -183,7 +200,7 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
                        su32(&mbar))
                    : "memory");
     }
-    load_tile(tile + gridDim.x);  // next operand rows in flight under the MMAs and the epilogue
+    load_tile(item + gridDim.x);  // next operand rows in flight under the MMAs and the epilogue
     mbar_wait(&mbar, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -196,7 +213,7 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
       if ((q >> 1) == h) {
         const int part = warp >> 2;  // two warps per lane quarter split the column chunks
         const int lr = (q & 1) * 32 + lane;
-        const int chunks = NP / 32 + ((NP & 31) ? 1 : 0);
+        const int chunks = NPS / 32 + ((NPS & 31) ? 1 : 0);
         for (int ci = part; ci < chunks; ci += UZ_THREADS / 128) {
           const int c0 = ci * 32;
           uint32_t r[32];
@@ -211,18 +228,18 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
                 "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
               : "r"(taddr));
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-          float* srow = stage + lr * N + c0;
-          if ((N & 3) == 0) {
+          float* srow = stage + lr * NS + c0;
+          if ((NS & 3) == 0) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
-              if (c0 + j < N)
+              if (c0 + j < NS)
                 *reinterpret_cast<float4*>(srow + j) =
                     make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
                                 __uint_as_float(r[j + 3]));
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (c0 + j < N) srow[j] = __uint_as_float(r[j]);
+              if (c0 + j < NS) srow[j] = __uint_as_float(r[j]);
           }
         }
       }
@@ -231,10 +248,16 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
       if (tid == 0) {
         const int r0 = m0 + 64 * h;
         const int nrows = min(64, M - r0);
-        if (nrows > 0) {
+        if (nrows > 0 && nsplit == 1) {
           float* dst = C + b * sC + (long long)r0 * N;
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
                        "r"(su32(stage)), "r"((uint32_t)(nrows * N * 4))
+                       : "memory");
+        } else if (nrows > 0) {
+          // rows beyond M are clipped by the TMA unit
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                           &tmC),
+                       "r"(half * NS), "r"(r0), "r"(b), "r"(su32(stage))
                        : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
@@ -263,7 +286,7 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
 // tiles; a tile's epilogue (tcgen05.ld, 16-byte stores of its rows) runs while the
 // next tile's chunks stream in.
 constexpr int ZP_KC = 32;
-constexpr int ZP_NBUF = 6;  // TMA ring depth
+constexpr int ZP_NBUF = 6;  // TMA ring depth (whole-band plans; 3 when B is large, e.g. config 4)
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
@@ -274,13 +297,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 
 constexpr int ZP_THREADS = 512;  // warp 0 TMA, warp 1 MMA, warps 4-7 epilogue, warps 8-15 split
-constexpr int ZP_NS = 4;         // small-part buffers
+constexpr int ZP_NS = 4;         // small-part buffers (2 with the shallow ring)
 
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
 }
 
-template <int NT>
+template <int NT, int NBUF, int NSB>
 __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                       const float* __restrict__ Bbig_c,
                                                                       const float* __restrict__ Bsm_c,
@@ -290,11 +313,11 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
   constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
   const uint32_t SBO_B = (uint32_t)(Kpad / 4) * 128;
   extern __shared__ __align__(1024) float sm[];
-  float* ring = sm;                     // ZP_NBUF chunks: TMA destination, split in place to big
-  float* smallb = ring + ZP_NBUF * CH;  // ZP_NS small chunks
-  float* Bb = smallb + ZP_NS * CH;
+  float* ring = sm;                     // NBUF chunks: TMA destination, split in place to big
+  float* smallb = ring + NBUF * CH;  // NSB small chunks
+  float* Bb = smallb + NSB * CH;
   float* Bs = Bb + NT * Kpad;
-  __shared__ __align__(8) unsigned long long full[ZP_NBUF], split_done[ZP_NBUF], mma_done[ZP_NBUF];
+  __shared__ __align__(8) unsigned long long full[NBUF], split_done[NBUF], mma_done[NBUF];
   __shared__ __align__(8) unsigned long long acc_full[2], acc_free[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -304,7 +327,7 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    for (int i = 0; i < ZP_NBUF; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;\n" ::"r"(su32(&split_done[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&mma_done[i])));
@@ -332,17 +355,17 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
 
   if (warp == 0) {
     if (lane == 0) {
-      // TMA producer: chunk q -> ring slot q % ZP_NBUF once chunk q - ZP_NBUF's MMAs are done
+      // TMA producer: chunk q -> ring slot q % NBUF once chunk q - NBUF's MMAs are done
       for (int q = 0; q < S; ++q) {
-        if (q >= ZP_NBUF) mbar_wait(&mma_done[q % ZP_NBUF], par(q - ZP_NBUF, ZP_NBUF));
+        if (q >= NBUF) mbar_wait(&mma_done[q % NBUF], par(q - NBUF, NBUF));
         const int tile = (int)blockIdx.x + (q / nk) * (int)gridDim.x, j = q % nk;
-        unsigned long long* bar = &full[q % ZP_NBUF];
+        unsigned long long* bar = &full[q % NBUF];
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
                      "r"((uint32_t)(CH * 4))
                      : "memory");
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-            "[%4];\n" ::"r"(su32(ring + (q % ZP_NBUF) * CH)),
+            "[%4];\n" ::"r"(su32(ring + (q % NBUF) * CH)),
             "l"(&tmA), "r"(j * ZP_KC), "r"(tile * 128), "r"(su32(bar))
             : "memory");
       }
@@ -354,10 +377,10 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
       for (int s = 0; s < S; ++s) {
         const int t = s / nk, j = s % nk;
         if (j == 0 && t >= 2) mbar_wait(&acc_free[t & 1], par(t - 2, 2));
-        mbar_wait(&split_done[s % ZP_NBUF], par(s, ZP_NBUF));
+        mbar_wait(&split_done[s % NBUF], par(s, NBUF));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t acc = tmem + (uint32_t)((t & 1) * NT);
-        const uint32_t a_big = su32(ring + (s % ZP_NBUF) * CH), a_sml = su32(smallb + (s % ZP_NS) * CH);
+        const uint32_t a_big = su32(ring + (s % NBUF) * CH), a_sml = su32(smallb + (s % NSB) * CH);
         const uint32_t b_off = (uint32_t)j * (ZP_KC / 4) * 128;
         const uint32_t b_big = su32(Bb) + b_off, b_sml = su32(Bs) + b_off;
         for (int pass = 0; pass < 3; ++pass) {
@@ -367,7 +390,7 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
                       (j | pass | ks) ? 1u : 0u);
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         su32(&mma_done[s % ZP_NBUF]))
+                         su32(&mma_done[s % NBUF]))
                      : "memory");
         if (j == nk - 1)
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -401,13 +424,13 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
       mbar_arrive(&acc_free[t & 1]);
     }
   } else if (warp >= 8) {
-    // split workers: chunk s in place -> TF32 big; small -> small buffer s % ZP_NS
+    // split workers: chunk s in place -> TF32 big; small -> small buffer s % NSB
     const int st = tid - 256;
     for (int s = 0; s < S; ++s) {
-      mbar_wait(&full[s % ZP_NBUF], par(s, ZP_NBUF));
-      if (s >= ZP_NS) mbar_wait(&mma_done[(s - ZP_NS) % ZP_NBUF], par(s - ZP_NS, ZP_NBUF));
-      float* big = ring + (s % ZP_NBUF) * CH;
-      float* sml = smallb + (s % ZP_NS) * CH;
+      mbar_wait(&full[s % NBUF], par(s, NBUF));
+      if (s >= NSB) mbar_wait(&mma_done[(s - NSB) % NBUF], par(s - NSB, NBUF));
+      float* big = ring + (s % NBUF) * CH;
+      float* sml = smallb + (s % NSB) * CH;
 #pragma unroll
       for (int u = 0; u < CH / 4 / 256; ++u) {
         const int e = st + u * 256;
@@ -421,7 +444,7 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
         reinterpret_cast<float4*>(sml)[e] = make_float4(a.x - bg.x, a.y - bg.y, a.z - bg.z, a.w - bg.w);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_arrive(&split_done[s % ZP_NBUF]);
+      mbar_arrive(&split_done[s % NBUF]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -446,8 +469,15 @@ __global__ void umma_zproj_prep_kernel(const float* __restrict__ Bbig, const flo
 
 int umma_zproject_kpad(int K) { return (K + ZP_KC - 1) / ZP_KC * ZP_KC; }
 
+static size_t umma_zproject_smem_ring(int N, int K, int nbuf, int ns) {
+  return ((size_t)2 * N * umma_zproject_kpad(K) + (size_t)(nbuf + ns) * 128 * ZP_KC) * sizeof(float);
+}
+
+// deep ring (6 TMA slots + 4 small buffers) when it fits, else the shallow one (3 + 2)
+static bool umma_zproject_deep(int N, int K) { return umma_zproject_smem_ring(N, K, ZP_NBUF, ZP_NS) <= 226 * 1024; }
+
 static size_t umma_zproject_smem(int N, int K) {
-  return ((size_t)2 * N * umma_zproject_kpad(K) + (size_t)(ZP_NBUF + ZP_NS) * 128 * ZP_KC) * sizeof(float);
+  return umma_zproject_deep(N, K) ? umma_zproject_smem_ring(N, K, ZP_NBUF, ZP_NS) : umma_zproject_smem_ring(N, K, 3, 2);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -492,7 +522,7 @@ void launch_umma_zproject(const float* A, const float* Bbig_c, const float* Bsm_
   const int mtiles = (M + 127) / 128;
   const int grid = std::min(kSMs, mtiles);
   auto go = [&](auto kern, int slot) {
-    static bool set[64][2] = {};
+    static bool set[64][4] = {};
     int dev = 0;
     LDDMM_CUDA(cudaGetDevice(&dev));
     if (!set[dev & 63][slot]) {
@@ -501,10 +531,11 @@ void launch_umma_zproject(const float* A, const float* Bbig_c, const float* Bsm_
     }
     kern<<<grid, ZP_THREADS, smem, s>>>(tm, Bbig_c, Bsm_c, C, M, umma_zproject_kpad(K));
   };
+  const bool deep = umma_zproject_deep(N, K);
   if (N == 32)
-    go(umma_zproject_kernel<32>, 0);
+    deep ? go(umma_zproject_kernel<32, ZP_NBUF, ZP_NS>, 0) : go(umma_zproject_kernel<32, 3, 2>, 2);
   else
-    go(umma_zproject_kernel<64>, 1);
+    deep ? go(umma_zproject_kernel<64, ZP_NBUF, ZP_NS>, 1) : go(umma_zproject_kernel<64, 3, 2>, 3);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -522,16 +553,30 @@ __global__ void umma_canon_b_kernel(const float* __restrict__ Bbig, const float*
 
 int umma_padded_n(int N) { return (N + 15) & ~15; }
 
-size_t umma_zembed_smem(int N, int K) {
-  const int NP = umma_padded_n(N);
-  return ((size_t)2 * NP * K + (size_t)2 * 128 * K + (size_t)128 * N) * sizeof(float);
+static size_t umma_zembed_smem_split(int N, int K, int nsplit) {
+  const int NPS = nsplit > 1 ? N / nsplit : umma_padded_n(N);
+  const int NS = nsplit > 1 ? N / nsplit : N;
+  return ((size_t)2 * NPS * K + (size_t)2 * 128 * K + (size_t)128 * NS) * sizeof(float);
 }
+
+// column slices per CTA: 1 (whole rows, 1-D bulk stores) when that plan fits, else 2 or 4
+// (each slice a multiple of 16 columns, TMA tensor stores)
+static int umma_zembed_nsplit(int N, int K) {
+  for (int ns : {1, 2, 4}) {
+    if (ns > 1 && (N % (16 * ns) != 0)) continue;
+    if (umma_zembed_smem_split(N, K, ns) <= 226 * 1024) return ns;
+  }
+  return 0;
+}
+
+size_t umma_zembed_smem(int N, int K) { return umma_zembed_smem_split(N, K, std::max(1, umma_zembed_nsplit(N, K))); }
 
 bool umma_zembed_fits(int N, int K) {
   // UMMA M = 128 needs N % 16 == 0 (padded), N <= 256; K a multiple of 8 and <= 64; the
-  // staged tile and operands must fit the 227 KB shared-memory budget; rows 16-byte aligned
-  return N >= 16 && umma_padded_n(N) <= 256 && K % 8 == 0 && K <= 64 && (K % 4) == 0 &&
-         umma_zembed_smem(N, K) <= 226 * 1024 && (N % 4) == 0;
+  // staged tile and operands must fit the 227 KB shared-memory budget (column slices
+  // when whole rows do not); rows 16-byte aligned
+  return N >= 16 && umma_padded_n(N) <= 256 && K % 8 == 0 && K <= 64 && (K % 4) == 0 && (N % 4) == 0 &&
+         umma_zembed_nsplit(N, K) > 0 && tensor_map_encoder() != nullptr;
 }
 
 void launch_umma_canon_b(const float* Bbig, const float* Bsm, int K, int N, float* Cbig, float* Csm,
@@ -544,9 +589,25 @@ void launch_umma_canon_b(const float* Bbig, const float* Bsm, int K, int N, floa
 void launch_umma_zembed(const float* A, long long sA, const float* Bbig_c, const float* Bsm_c, float* C,
                         long long sC, int M, int N, int K, int nb, cudaStream_t s) {
   const int NP = umma_padded_n(N);
-  const size_t smem = umma_zembed_smem(N, K);
+  const int nsplit = umma_zembed_nsplit(N, K);
+  if (nsplit < 1) throw EngineError(3, "umma z-embed: no shared-memory plan for N = " + std::to_string(N));
+  const size_t smem = umma_zembed_smem_split(N, K, nsplit);
   const int mtiles = (M + 127) / 128;
-  const int grid = std::min(kSMs, mtiles * nb);
+  // a multiple of nsplit, so every CTA keeps one column slice
+  const int grid = std::min(kSMs / nsplit * nsplit, mtiles * nb * nsplit);
+  CUtensorMap tmC;
+  std::memset(&tmC, 0, sizeof(tmC));
+  if (nsplit > 1) {
+    const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)nb};
+    const cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)sC * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)(N / nsplit), 64, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = tensor_map_encoder()(&tmC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, strides, box, estr,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      throw EngineError(3, "umma z-embed: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  }
   auto go = [&](auto kern, int slot) {  // one attribute flag per instantiation (same pointer type)
     static bool set[64][4] = {};
     int dev = 0;
@@ -555,13 +616,14 @@ void launch_umma_zembed(const float* A, long long sA, const float* Bbig_c, const
       LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
       set[dev & 63][slot] = true;
     }
-    kern<<<grid, UZ_THREADS, smem, s>>>(A, sA, Bbig_c, Bsm_c, C, sC, M, N, NP, K, nb);
+    kern<<<grid, UZ_THREADS, smem, s>>>(A, sA, Bbig_c, Bsm_c, C, sC, M, N, NP, K, nb, nsplit, tmC);
   };
-  if (NP <= 32)
+  const int NPS = nsplit > 1 ? N / nsplit : NP;
+  if (NPS <= 32)
     go(umma_zembed_kernel<32>, 0);
-  else if (NP <= 64)
+  else if (NPS <= 64)
     go(umma_zembed_kernel<64>, 1);
-  else if (NP <= 128)
+  else if (NPS <= 128)
     go(umma_zembed_kernel<128>, 2);
   else
     go(umma_zembed_kernel<256>, 3);

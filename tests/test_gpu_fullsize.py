@@ -1,11 +1,21 @@
-"""Full-size parity against the REFERENCE itself: the GN-Krylov history and final
-velocity of BASELINE.json's configs, produced once by the unmodified reference
-(oracle/_ref, tools/ref_config2_golden.py — hours of CPU) and committed as
-tests/golden/config{1,2}_ref.npz.  The engine reruns the same registration on the
-GPU (fp32 grids, fp64 band algebra) and must take the same path: identical GN
-iteration count, PCG iteration counts, step lengths and stop reason; per-iteration
-energies within 1e-4 relative; final velocity within 1e-3 relative L2; the
-deformation Jacobian range within 1e-3 (optimizer.hpp:143-262, metrics.hpp:24-79).
+"""Full-size parity against the REFERENCE itself.  The GN-Krylov histories and final
+velocities of BASELINE.json's configs were produced once by the unmodified reference
+(oracle/_ref; tools/ref_config2_golden.py and tools/ref_fullsize_golden.py — hours of
+CPU) and committed as tests/golden/config*_ref.npz:
+
+  config1                     64^3 sphere -> ellipsoid, K = 16, nt = 10, deformation-state
+  config2                     180x210x180 brain-like pair, K = 32, nt = 10, deformation-state
+  config3_original            the config-2 pair, `original` (image-state) variant
+  config3_state_equation      the config-2 pair, `state_equation` variant
+  config4_ops                 256^3, K = 64, nt = 20: forward (with adjoint), gradient and one
+                              Hessian-vector product on a fixed seeded velocity
+
+The engine reruns them on the GPU (fp32 grids, fp64 band algebra) and must take the
+same path with the SURVEY.md §8(c) tolerances: identical GN iteration count, PCG
+iterations, step lengths and stop reason; E, E_data, E_reg per iteration within 1e-5
+relative; mse_rel within 1e-5 absolute; final velocity within 1e-4 relative L2; the
+Jacobian-determinant ranges within 1e-4 (optimizer.hpp:143-262, metrics.hpp:24-79,
+variants.hpp:262-547).  The achieved errors are printed (pytest -s).
 """
 import os
 
@@ -28,27 +38,76 @@ def pair(tag, dims):
     return phantoms.brain_pair(dims, seed=2006)
 
 
-@pytest.mark.parametrize("tag", ["config1", "config2"])
-def test_registration_matches_reference(cuda, tag):
+def relerr(x, ref):
+    return abs(x - ref) / abs(ref) if ref != 0 else abs(x)
+
+
+@pytest.mark.parametrize("tag,variant", [("config1", "deformation_state_equation"),
+                                         ("config2", "deformation_state_equation"),
+                                         ("config3_original", "original"),
+                                         ("config3_state_equation", "state_equation")])
+def test_registration_matches_reference(cuda, tag, variant):
     path = os.path.join(GOLD, f"{tag}_ref.npz")
     if not os.path.exists(path):
-        pytest.skip(f"{tag}_ref.npz not generated (tools/ref_config2_golden.py)")
+        pytest.skip(f"{tag}_ref.npz not generated (tools/ref_fullsize_golden.py)")
     from paper_2006_06823_b200 import lddmm as L
     z = np.load(path)
     dims, band = tuple(int(x) for x in z["dims"]), tuple(int(x) for x in z["band"])
     I0, I1 = pair(tag, dims)
-    m = L.Model(L.BandSpec(L.GridSpec(dims), band), I0, I1, "deformation_state_equation", int(z["nt"]),
-                float(z["sigma2"]))
+    m = L.Model(L.BandSpec(L.GridSpec(dims), band), I0, I1, variant, int(z["nt"]), float(z["sigma2"]))
     res = L.optimize(m, None, L.OptimizeOptions(max_iter=10, pcg_max_iter=5))
     hist = z["history"]
     assert L.STOP_REASONS.index(res.stop) == int(z["stop"])
     assert res.iterations == int(z["iterations"])
     assert len(res.history) == hist.shape[0]
+    worst = dict(E=0.0, E_data=0.0, E_reg=0.0, mse=0.0)
     for r, row in zip(res.history, hist):
         assert r.pcg_iters == int(row[6]) and r.pcg_fallback == bool(row[7]) and r.epsilon == row[8]
-        assert abs(r.energy - row[1]) <= 1e-4 * abs(row[1])
-        assert abs(r.energy_data - row[2]) <= 1e-4 * abs(row[2])
-        assert abs(r.mse_rel - row[4]) <= 1e-4
-    assert rel(res.v.numpy(), z["v"]) < 1e-3
+        worst["E"] = max(worst["E"], relerr(r.energy, row[1]))
+        worst["E_data"] = max(worst["E_data"], relerr(r.energy_data, row[2]))
+        worst["E_reg"] = max(worst["E_reg"], relerr(r.energy_reg, row[3]))
+        worst["mse"] = max(worst["mse"], abs(r.mse_rel - row[4]))
+    ev = rel(res.v.numpy(), z["v"])
     _, _, jac = L.compute_maps(m, res.v)
-    assert np.allclose(jac, z["jac"], rtol=1e-3, atol=1e-3)
+    ej = float(np.max(np.abs(jac - z["jac"])))
+    print(f"{tag}: GN {res.iterations} stop {res.stop}; max rel E {worst['E']:.1e} E_data {worst['E_data']:.1e} "
+          f"E_reg {worst['E_reg']:.1e}; mse abs {worst['mse']:.1e}; velocity rel-L2 {ev:.1e}; Jacobian abs {ej:.1e}")
+    assert worst["E"] <= 1e-5 and worst["E_data"] <= 1e-5 and worst["E_reg"] <= 1e-5
+    assert worst["mse"] <= 1e-5
+    assert ev <= 1e-4
+    assert ej <= 1e-4
+
+
+def test_config4_ops_match_reference(cuda):
+    """BASELINE config 4 (256^3, K = 64, nt = 20, deformation-state): one forward with
+    adjoint, the gradient and one Hessian-vector product on the reference's own fixed
+    inputs (v, dv from synth.hpp's random_band_field with the seeds in the fixture),
+    against the reference's values: energies 1e-5 relative, u(1) / gradient / hessvec
+    1e-4 relative L2 (variants.hpp:262-344, transport.hpp:264-298)."""
+    path = os.path.join(GOLD, "config4_ops_ref.npz")
+    if not os.path.exists(path):
+        pytest.skip("config4_ops_ref.npz not generated (tools/ref_fullsize_golden.py config4)")
+    from oracle import ref
+    from paper_2006_06823_b200 import lddmm as L
+    z = np.load(path)
+    dims, band, nt = tuple(int(x) for x in z["dims"]), tuple(int(x) for x in z["band"]), int(z["nt"])
+    if "v" in z.files:
+        v, dv = z["v"], z["dv"]
+    else:  # regenerated with the reference's own generator (oracle/_ref)
+        v = ref.random_band_field(dims, (1.0, 1.0, 1.0), band, int(z["v_seed"]), float(z["v_amp"]),
+                                  float(z["v_k0"]))[None]
+        dv = ref.random_band_field(dims, (1.0, 1.0, 1.0), band, int(z["dv_seed"]), float(z["dv_amp"]),
+                                   float(z["dv_k0"]))[None]
+    I0, I1 = pair("config4", dims)
+    m = L.Model(L.BandSpec(L.GridSpec(dims), band), I0, I1, "deformation_state_equation", nt, float(z["sigma2"]))
+    e = m.forward(m.velocity(v), True)
+    er = [relerr(e[k], z["energy"][i]) for i, k in enumerate(("energy", "energy_reg", "energy_data"))]
+    u1 = m.series("u")[-1]
+    g = m.gradient().numpy()
+    hv = m.hessvec(m.velocity(dv)).numpy()
+    eu, eg, eh = rel(u1, z["u_final"]), rel(g, z["gradient"]), rel(hv, z["hessvec"])
+    print(f"config4: rel E {er[0]:.1e} E_reg {er[1]:.1e} E_data {er[2]:.1e}; cfl {e['cfl']:.4f} "
+          f"(ref {z['energy'][3]:.4f}); u(1) {eu:.1e}, gradient {eg:.1e}, hessvec {eh:.1e}")
+    assert max(er) <= 1e-5
+    assert abs(e["cfl"] - z["energy"][3]) <= 1e-5 * max(1.0, abs(z["energy"][3]))
+    assert eu <= 1e-4 and eg <= 1e-4 and eh <= 1e-4
