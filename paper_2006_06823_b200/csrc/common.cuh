@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -41,6 +42,19 @@ inline long long& launch_counter() {
     ++::lddmm_b200::launch_counter();           \
     LDDMM_CUDA(cudaGetLastError());             \
   } while (0)
+
+// NVTX range for the host-side phases (forward / gradient / hessvec / GN iteration /
+// PCG): visible in any NVTX-aware profiler timeline; header-only (nvtx3), no-ops when
+// no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define LDDMM_NVTX_CAT2(a, b) a##b
+#define LDDMM_NVTX_CAT(a, b) LDDMM_NVTX_CAT2(a, b)
+#define LDDMM_NVTX(name) ::lddmm_b200::NvtxRange LDDMM_NVTX_CAT(nvtx_range_, __LINE__)(name)
 
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
 

@@ -780,6 +780,7 @@ double Engine::reg_energy(const double2* v) {  // variants.hpp:280-287
 }
 
 Energies Engine::forward(const double2* v, bool with_adjoint) {
+  LDDMM_NVTX(with_adjoint ? "forward+adjoint" : "forward");
   const long long V = vec_elems(), N = npts();
   have_cache_ = false;
   provider_build(v, prov_, with_adjoint);
@@ -811,6 +812,7 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
 }
 
 double Engine::energy(const double2* v) {
+  LDDMM_NVTX("energy (trial)");
   if (prob_.variant == 0) return energy_original(v);
   provider_build(v, trial_prov_, false);
   solve_displacement_fwd(trial_prov_, nullptr, false, bt(11));
@@ -821,6 +823,7 @@ double Engine::energy(const double2* v) {
 }
 
 void Engine::gradient(double2* out) {
+  LDDMM_NVTX("gradient");
   shape_require(have_cache_ && cache_adjoint_, "gradient requires an adjoint-enabled forward cache");
   if (prob_.variant == 2)
     assemble_jacT_terms(u_.p, rho_.p, prov_.v.p, out);
@@ -829,6 +832,7 @@ void Engine::gradient(double2* out) {
 }
 
 void Engine::hessvec(const double2* dv, double2* out) {
+  LDDMM_NVTX("hessvec");
   shape_require(have_cache_ && cache_adjoint_, "hessvec requires an adjoint-enabled forward cache");
   if (prob_.variant == 0) return hessvec_original(dv, out);
   if (prob_.variant == 1) return hessvec_state(dv, out);

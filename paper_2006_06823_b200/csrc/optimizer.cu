@@ -33,6 +33,7 @@ struct Workspace {  // views of the engine's persistent optimizer workspace
 // optimizer.hpp:86-120; x = 0, r = rhs, z = L^-1 r, p = z
 void pcg_solve(Engine& e, Workspace& w, const double2* rhs, int max_iter, double tol, PcgInfo& info,
                OptimizeResult& res) {
+  LDDMM_NVTX("pcg_solve");
   info = PcgInfo{};
   const long long n = e.vel_elems();
   e.tv_scaled(rhs, 0.0, w.x.p);
@@ -111,6 +112,7 @@ OptimizeResult optimize(Engine& e, double2* v, const OptimizeOptions& opt) {
 
   double e_prev = c.energy;
   for (int iter = 1; iter <= opt.max_iter; ++iter) {
+    LDDMM_NVTX("GN iteration");
     const double t0 = now_ms();
     PcgInfo pcg;
     e.tv_scaled(w.g.p, -1.0, w.rhs.p);
