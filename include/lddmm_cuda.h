@@ -116,10 +116,11 @@ int lddmm_sync(lddmm_ctx* ctx);
 long long lddmm_launch_count(void); /* kernels launched by this library (process-wide) */
 /* the context's CUDA stream (cudaStream_t), for events / external synchronisation */
 void* lddmm_stream(lddmm_ctx* ctx);
-/* live SL-gather timing: CUDA events around every gather launch while on;
- * stats = device ms summed over launches, launch count, algorithmic bytes
- * sum of N * (12 + 8 C) */
-int lddmm_gather_timing(lddmm_ctx* ctx, int on);
+/* live timing (measurement only): mode bit 0 = CUDA events around every SL-gather
+ * launch, bit 1 = around every full-grid truncated-DFT call; 0 = off (resets the
+ * window).  gather stats = device ms summed over launches, launch count, algorithmic
+ * bytes sum of N * (12 + 8 C) */
+int lddmm_gather_timing(lddmm_ctx* ctx, int mode);
 int lddmm_gather_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* bytes);
 /* same timing window: full-grid truncated DFT calls (embed / project pipelines of nf
  * fields), with their algorithmic flops (8 (y + x stage complex MACs)

@@ -169,8 +169,8 @@ long long lddmm_launch_count(void) { return launch_counter(); }
 
 void* lddmm_stream(lddmm_ctx* ctx) { return (void*)ctx->eng->stream(); }
 
-int lddmm_gather_timing(lddmm_ctx* ctx, int on) {
-  return guard(ctx, [&] { ctx->eng->set_gather_timing(on != 0); });
+int lddmm_gather_timing(lddmm_ctx* ctx, int mode) {
+  return guard(ctx, [&] { ctx->eng->set_gather_timing(mode); });
 }
 
 int lddmm_gather_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* bytes) {

@@ -247,7 +247,7 @@ void Engine::timing_end(int kind, double amount) {
 }
 
 void Engine::timed_gather(const float* coef, int ncomp, const float* dep, float* out) {
-  if (!gt_on_) {
+  if (!(gt_on_ & 1)) {
     launch_gather_cubic(coef, ncomp, dep, out, full_.N, stream_);
     return;
   }
@@ -266,8 +266,8 @@ double Engine::dft_flops_per_field() const {
   return 8.0 * (Kx * H * Ky * Ny + Ny * H * Kx * Nx) + 4.0 * Nx * Ny * Nz * H;
 }
 
-void Engine::set_gather_timing(bool on) {
-  gt_on_ = on;
+void Engine::set_gather_timing(int mode) {
+  gt_on_ = mode;
   gt_used_ = 0;
 }
 
@@ -365,7 +365,7 @@ double Engine::mse_denominator() { return mse_denom_; }
 // generic pipelines
 
 void Engine::embed_fields(const DftPlan& p, const PrepArgs& a, float* out, float2* D, float2* E1, float2* E2) {
-  const bool timed = gt_on_ && &p == &full_;
+  const bool timed = (gt_on_ & 2) && &p == &full_;
   if (timed) timing_begin();
   dft_embed_prep(p, a, D, E1, E2, out, stream_);
   if (timed) timing_end(1, a.nf * dft_flops_per_field());
@@ -373,7 +373,7 @@ void Engine::embed_fields(const DftPlan& p, const PrepArgs& a, float* out, float
 
 void Engine::project_fields(const DftPlan& p, const float* f, const FinArgs& a, float2* G1, float2* G2,
                             float2* G3) {
-  const bool timed = gt_on_ && &p == &full_;
+  const bool timed = (gt_on_ & 2) && &p == &full_;
   if (timed) timing_begin();
   dft_project_fin(p, f, a, G1, G2, G3, stream_);
   if (timed) timing_end(1, a.nf * dft_flops_per_field());

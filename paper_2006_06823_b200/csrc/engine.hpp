@@ -160,7 +160,7 @@ class Engine {
   // Live per-launch timing of the SL gather kernel (CUDA events on the engine
   // stream around every gather launch while enabled).  stats: total device ms,
   // launch count, algorithmic bytes N * (12 + 8 C) summed over launches.
-  void set_gather_timing(bool on);
+  void set_gather_timing(int mode);  // bit 0 gathers, bit 1 full-grid DFTs
   void gather_stats(double* ms, long long* launches, double* bytes);
   // kind 0: SL gathers (amount = algorithmic bytes), 1: full-grid truncated DFTs (flops)
   void timing_stats(int kind, double* ms, long long* launches, double* amount);
@@ -309,7 +309,7 @@ class Engine {
   double reduce(int nparts, int op);
   void timed_gather(const float* coef, int ncomp, const float* dep, float* out);
 
-  bool gt_on_ = false;
+  int gt_on_ = 0;
   std::vector<cudaEvent_t> gt_events_;
   std::vector<double> gt_bytes_;
   std::vector<int> gt_kind_;

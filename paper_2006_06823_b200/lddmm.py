@@ -310,8 +310,9 @@ class Context:
     def sync(self):
         self.check(lib().lddmm_sync(self.h))
 
-    def gather_timing(self, on=True):
-        self.check(lib().lddmm_gather_timing(self.h, int(on)))
+    def gather_timing(self, on=True, dft=False):
+        """CUDA events around every SL gather (and, with dft=True, every full-grid DFT call)."""
+        self.check(lib().lddmm_gather_timing(self.h, (1 if on else 0) | (2 if dft else 0)))
 
     def gather_stats(self):
         ms, n, b = C.c_double(), C.c_longlong(), C.c_double()

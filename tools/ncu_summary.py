@@ -10,7 +10,11 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__data_bank_confli
        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smsp__sass_inst_executed_op_shared_ld.sum",
        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
        "smsp__inst_executed.sum", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
+       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+       "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__pipe_tmem_cycles_active.avg.pct_of_peak_sustained_active",
+       "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
 
 
 def main(rep):
