@@ -15,6 +15,12 @@ using namespace lddmm_b200;
 struct lddmm_ctx {
   std::unique_ptr<Engine> eng;
   std::string err;
+  // d = 2: the engine runs the 3-D problem (Nx, Ny, zr) (Problem::zrep); the ABI keeps
+  // the reference's 2-D layouts and converts at the boundary (grid fields: replicate
+  // along z / take the z = 0 slice; vectors: 2 components; band vectors: the kz = 0
+  // plane scaled by zr, components x, y)
+  int d = 3;
+  int zr = 1;
 };
 
 namespace {
@@ -54,6 +60,71 @@ int guard(lddmm_ctx* ctx, F&& f, int* step = nullptr) {
 
 inline double2* D2(double* p) { return reinterpret_cast<double2*>(p); }
 inline const double2* D2(const double* p) { return reinterpret_cast<const double2*>(p); }
+
+// ---- 2-D <-> internal 3-D layout conversions (lddmm_ctx::d == 2) -------------------
+
+constexpr int kZRep2D = 4;  // z replicas of a 2-D problem (even, >= 4, a multiple of 4)
+
+long long n2d(const lddmm_ctx* ctx) {
+  const Problem& p = ctx->eng->problem();
+  return (long long)p.dims[0] * p.dims[1];
+}
+
+// host grid components: 2-D [nc][Nx*Ny] -> 3-D [nc3][Nx*Ny*zr] (z-constant; components
+// nc .. nc3-1 zero)
+std::vector<double> grid_to3(const lddmm_ctx* ctx, const double* src, int nc, int nc3) {
+  const long long n2 = n2d(ctx), n3 = n2 * ctx->zr;
+  std::vector<double> out((size_t)nc3 * n3, 0.0);
+  for (int c = 0; c < nc; ++c)
+    for (long long i = 0; i < n2; ++i)
+      for (int z = 0; z < ctx->zr; ++z) out[(size_t)c * n3 + i * ctx->zr + z] = src[(size_t)c * n2 + i];
+  return out;
+}
+
+// host 3-D [nc3][n3] -> 2-D [nc][n2] (the z = 0 slice of the first nc components)
+void grid_to2(const lddmm_ctx* ctx, const double* src, int nc, double* dst) {
+  const long long n2 = n2d(ctx), n3 = n2 * ctx->zr;
+  for (int c = 0; c < nc; ++c)
+    for (long long i = 0; i < n2; ++i) dst[(size_t)c * n2 + i] = src[(size_t)c * n3 + i * ctx->zr];
+}
+
+// band vectors: 2-D [nodes][2][Kx][Ky] complex <-> 3-D [nodes][3][Kx][Ky][Kz]
+void band_to3(const lddmm_ctx* ctx, const double* src, int nodes, double* dst) {
+  const Problem& p = ctx->eng->problem();
+  const long long kxy = (long long)p.band[0] * p.band[1], kz = p.band[2];
+  const long long v2 = 2 * kxy, v3 = 3 * kxy * kz;
+  std::memset(dst, 0, (size_t)nodes * v3 * 2 * sizeof(double));
+  for (int nd = 0; nd < nodes; ++nd)
+    for (int c = 0; c < 2; ++c)
+      for (long long k = 0; k < kxy; ++k) {
+        const double* s = src + 2 * (nd * v2 + c * kxy + k);
+        double* o = dst + 2 * (nd * v3 + (c * kxy + k) * kz);  // kz = 0 entry
+        o[0] = ctx->zr * s[0];
+        o[1] = ctx->zr * s[1];
+      }
+}
+
+void band_to2(const lddmm_ctx* ctx, const double* src, int nodes, double* dst) {
+  const Problem& p = ctx->eng->problem();
+  const long long kxy = (long long)p.band[0] * p.band[1], kz = p.band[2];
+  const long long v2 = 2 * kxy, v3 = 3 * kxy * kz;
+  for (int nd = 0; nd < nodes; ++nd)
+    for (int c = 0; c < 2; ++c)
+      for (long long k = 0; k < kxy; ++k) {
+        const double* s = src + 2 * (nd * v3 + (c * kxy + k) * kz);
+        double* o = dst + 2 * (nd * v2 + c * kxy + k);
+        o[0] = s[0] / ctx->zr;
+        o[1] = s[1] / ctx->zr;
+      }
+}
+
+int vel_nodes(const lddmm_ctx* ctx) { return (int)(ctx->eng->vel_elems() / ctx->eng->vec_elems()); }
+
+__global__ void replicate_z_kernel(const float* __restrict__ src, long long n2, int zr, float* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2 * zr;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i / zr];
+}
 
 OptimizeOptions to_opts(const lddmm_options* o) {
   OptimizeOptions r;
@@ -128,12 +199,22 @@ int lddmm_create(const lddmm_problem* p, int device, lddmm_ctx** out) {
   DeviceScope restore(caller_dev);  // the Engine constructor binds `device`
   const int rc = guard(ctx.get(), [&] {
     shape_require(p != nullptr, "null problem");
-    shape_require(p->d == 3, "only 3-D grids are supported by the CUDA engine");
+    shape_require(p->d == 3 || p->d == 2, "grid dimension must be 2 or 3 (core.hpp:49-52)");
     Problem q;
     for (int a = 0; a < 3; ++a) {
       q.dims[a] = p->dims[a];
       q.spacing[a] = p->spacing[a];
       q.band[a] = p->band[a];
+    }
+    if (p->d == 2) {
+      // z replicated kZRep2D times at spacing 1 / kZRep2D (Problem::zrep)
+      q.dims[2] = kZRep2D;
+      q.spacing[2] = 1.0 / kZRep2D;
+      q.band[2] = kZRep2D;
+      q.d = 2;
+      q.zrep = kZRep2D;
+      ctx->d = 2;
+      ctx->zr = kZRep2D;
     }
     q.nt = p->nt;
     q.variant = p->variant;
@@ -182,14 +263,41 @@ int lddmm_dft_stats(lddmm_ctx* ctx, double* ms, long long* launches, double* flo
 }
 
 int lddmm_set_images(lddmm_ctx* ctx, const double* I0, const double* I1) {
-  return guard(ctx, [&] { ctx->eng->set_images_host(I0, I1); });
+  return guard(ctx, [&] {
+    if (ctx->d == 2) {
+      const std::vector<double> a = grid_to3(ctx, I0, 1, 1), b = grid_to3(ctx, I1, 1, 1);
+      ctx->eng->set_images_host(a.data(), b.data());
+    } else {
+      ctx->eng->set_images_host(I0, I1);
+    }
+  });
 }
 
 int lddmm_set_images_dev_f32(lddmm_ctx* ctx, const float* I0, const float* I1) {
-  return guard(ctx, [&] { ctx->eng->set_images_device_f32(I0, I1); });
+  return guard(ctx, [&] {
+    if (ctx->d == 2) {
+      Engine& e = *ctx->eng;
+      const long long n2 = n2d(ctx);
+      DevBuf<float> a(n2 * ctx->zr), b(n2 * ctx->zr);
+      replicate_z_kernel<<<grid_for(n2 * ctx->zr, 256), 256, 0, e.stream()>>>(I0, n2, ctx->zr, a.p);
+      LDDMM_LAUNCH_CHECK();
+      replicate_z_kernel<<<grid_for(n2 * ctx->zr, 256), 256, 0, e.stream()>>>(I1, n2, ctx->zr, b.p);
+      LDDMM_LAUNCH_CHECK();
+      e.set_images_device_f32(a.p, b.p);
+      e.sync();
+    } else {
+      ctx->eng->set_images_device_f32(I0, I1);
+    }
+  });
 }
 
-long long lddmm_velocity_doubles(const lddmm_ctx* ctx) { return 2 * ctx->eng->vel_elems(); }
+long long lddmm_velocity_doubles(const lddmm_ctx* ctx) {
+  if (ctx->d == 2) {
+    const Problem& p = ctx->eng->problem();
+    return 2LL * vel_nodes(ctx) * 2 * p.band[0] * p.band[1];
+  }
+  return 2 * ctx->eng->vel_elems();
+}
 
 int lddmm_vel_alloc(lddmm_ctx* ctx, double** v) {
   return guard(ctx, [&] {
@@ -206,16 +314,30 @@ int lddmm_vel_free(lddmm_ctx* ctx, double* v) {
 
 int lddmm_vel_upload(lddmm_ctx* ctx, double* dv, const double* hv) {
   return guard(ctx, [&] {
-    LDDMM_CUDA(cudaMemcpyAsync(dv, hv, ctx->eng->vel_elems() * sizeof(double2), cudaMemcpyHostToDevice,
-                               ctx->eng->stream()));
+    const size_t bytes = ctx->eng->vel_elems() * sizeof(double2);
+    if (ctx->d == 2) {
+      std::vector<double> t(2 * ctx->eng->vel_elems());
+      band_to3(ctx, hv, vel_nodes(ctx), t.data());
+      LDDMM_CUDA(cudaMemcpyAsync(dv, t.data(), bytes, cudaMemcpyHostToDevice, ctx->eng->stream()));
+      ctx->eng->sync();
+      return;
+    }
+    LDDMM_CUDA(cudaMemcpyAsync(dv, hv, bytes, cudaMemcpyHostToDevice, ctx->eng->stream()));
     ctx->eng->sync();
   });
 }
 
 int lddmm_vel_download(lddmm_ctx* ctx, const double* dv, double* hv) {
   return guard(ctx, [&] {
-    LDDMM_CUDA(cudaMemcpyAsync(hv, dv, ctx->eng->vel_elems() * sizeof(double2), cudaMemcpyDeviceToHost,
-                               ctx->eng->stream()));
+    const size_t bytes = ctx->eng->vel_elems() * sizeof(double2);
+    if (ctx->d == 2) {
+      std::vector<double> t(2 * ctx->eng->vel_elems());
+      LDDMM_CUDA(cudaMemcpyAsync(t.data(), dv, bytes, cudaMemcpyDeviceToHost, ctx->eng->stream()));
+      ctx->eng->sync();
+      band_to2(ctx, t.data(), vel_nodes(ctx), hv);
+      return;
+    }
+    LDDMM_CUDA(cudaMemcpyAsync(hv, dv, bytes, cudaMemcpyDeviceToHost, ctx->eng->stream()));
     ctx->eng->sync();
   });
 }
@@ -274,21 +396,27 @@ int lddmm_precondition(lddmm_ctx* ctx, const double* in, double* out) {
   });
 }
 
+// device fp32 grid components -> host fp64 in the ABI layout (2-D: the z = 0 slice)
+static void fetch_grid(lddmm_ctx* ctx, const float* dev, int nc, double* host) {
+  Engine& e = *ctx->eng;
+  const long long N = e.npts();
+  DevBuf<double> tmp(nc * N);
+  launch_f32_to_f64(nc * N, dev, tmp.p, e.stream());
+  if (ctx->d == 2) {
+    std::vector<double> t(nc * N);
+    LDDMM_CUDA(cudaMemcpyAsync(t.data(), tmp.p, nc * N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+    e.sync();
+    grid_to2(ctx, t.data(), nc, host);
+    return;
+  }
+  LDDMM_CUDA(cudaMemcpyAsync(host, tmp.p, nc * N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
+  e.sync();
+}
+
 int lddmm_get_fields(lddmm_ctx* ctx, double* m1, double* res) {
   return guard(ctx, [&] {
-    Engine& e = *ctx->eng;
-    const long long N = e.npts();
-    DevBuf<double> tmp(N);
-    if (m1) {
-      launch_f32_to_f64(N, e.m1(), tmp.p, e.stream());
-      LDDMM_CUDA(cudaMemcpyAsync(m1, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
-      e.sync();
-    }
-    if (res) {
-      launch_f32_to_f64(N, e.residual(), tmp.p, e.stream());
-      LDDMM_CUDA(cudaMemcpyAsync(res, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
-      e.sync();
-    }
+    if (m1) fetch_grid(ctx, ctx->eng->m1(), 1, m1);
+    if (res) fetch_grid(ctx, ctx->eng->residual(), 1, res);
   });
 }
 
@@ -298,10 +426,8 @@ int lddmm_get_grid(lddmm_ctx* ctx, int which, double* host_out) {
     const long long N = e.npts();
     const float* src = e.grid_field(which);
     shape_require(src != nullptr, "lddmm_get_grid: unknown field");
-    DevBuf<double> tmp(N);
-    launch_f32_to_f64(N, src, tmp.p, e.stream());
-    LDDMM_CUDA(cudaMemcpyAsync(host_out, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
-    e.sync();
+    (void)N;
+    fetch_grid(ctx, src, 1, host_out);
   });
 }
 
@@ -311,6 +437,12 @@ int lddmm_get_series(lddmm_ctx* ctx, int which, double* host_out) {
     const long long n = (e.problem().nt + 1) * e.vec_elems();
     DevBuf<double2> tmp(n);
     e.series(which, tmp.p);
+    if (ctx->d == 2) {
+      std::vector<double> t(2 * n);
+      LDDMM_CUDA(cudaMemcpy(t.data(), tmp.p, n * sizeof(double2), cudaMemcpyDeviceToHost));
+      band_to2(ctx, t.data(), e.problem().nt + 1, host_out);
+      return;
+    }
     LDDMM_CUDA(cudaMemcpy(host_out, tmp.p, n * sizeof(double2), cudaMemcpyDeviceToHost));
   });
 }
@@ -328,12 +460,23 @@ int lddmm_register(lddmm_ctx* ctx, const double* I0, const double* I1, const ldd
                    lddmm_iteration_record* hist, int cap, lddmm_result* res) {
   return guard(ctx, [&] {
     Engine& e = *ctx->eng;
-    e.set_images_host(I0, I1);
+    if (ctx->d == 2) {
+      const std::vector<double> a = grid_to3(ctx, I0, 1, 1), b = grid_to3(ctx, I1, 1, 1);
+      e.set_images_host(a.data(), b.data());
+    } else {
+      e.set_images_host(I0, I1);
+    }
     double2* v = e.register_velocity();
     LDDMM_CUDA(cudaMemsetAsync(v, 0, e.vel_elems() * sizeof(double2), e.stream()));
     OptimizeResult r = optimize(e, v, to_opts(opt));
-    if (host_v)
+    if (host_v && ctx->d == 2) {
+      std::vector<double> t(2 * e.vel_elems());
+      LDDMM_CUDA(cudaMemcpyAsync(t.data(), v, e.vel_elems() * sizeof(double2), cudaMemcpyDeviceToHost, e.stream()));
+      e.sync();
+      band_to2(ctx, t.data(), vel_nodes(ctx), host_v);
+    } else if (host_v) {
       LDDMM_CUDA(cudaMemcpyAsync(host_v, v, e.vel_elems() * sizeof(double2), cudaMemcpyDeviceToHost, e.stream()));
+    }
     e.sync();
     fill_result(r, hist, cap, res);
   });
@@ -345,17 +488,9 @@ int lddmm_maps(lddmm_ctx* ctx, const double* v, double* hf, double* hi, double j
     const long long N = e.npts();
     DevBuf<float> f(3 * N), i(3 * N);
     e.maps(D2(v), f.p, i.p, jac);
-    DevBuf<double> t(3 * N);
-    if (hf) {
-      launch_f32_to_f64(3 * N, f.p, t.p, e.stream());
-      LDDMM_CUDA(cudaMemcpyAsync(hf, t.p, 3 * N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
-      e.sync();
-    }
-    if (hi) {
-      launch_f32_to_f64(3 * N, i.p, t.p, e.stream());
-      LDDMM_CUDA(cudaMemcpyAsync(hi, t.p, 3 * N * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
-      e.sync();
-    }
+    const int nc = ctx->d;  // 2-D: the x, y displacement components
+    if (hf) fetch_grid(ctx, f.p, nc, hf);
+    if (hi) fetch_grid(ctx, i.p, nc, hi);
   });
 }
 
@@ -478,12 +613,6 @@ void upload_f32(Engine& e, const double* host, long long n, float* dev) {
   e.sync();
 }
 
-void download_f64(Engine& e, const float* dev, long long n, double* host) {
-  DevBuf<double> t(n);
-  launch_f32_to_f64(n, dev, t.p, e.stream());
-  LDDMM_CUDA(cudaMemcpyAsync(host, t.p, n * sizeof(double), cudaMemcpyDeviceToHost, e.stream()));
-  e.sync();
-}
 
 }  // namespace
 
@@ -513,13 +642,19 @@ int lddmm_warp(lddmm_ctx* ctx, int kind, const double* field, int ncomp, const d
                   "lddmm_warp: kind must be LDDMM_INTERP_CUBIC or LDDMM_INTERP_NEAREST");
     shape_require(ncomp >= 1 && ncomp <= 6, "lddmm_warp: 1..6 components");
     DevBuf<float> f(ncomp * N), d(3 * N), o(ncomp * N);
-    upload_f32(e, field, ncomp * N, f.p);
-    upload_f32(e, disp, 3 * N, d.p);
+    if (ctx->d == 2) {
+      const std::vector<double> f3 = grid_to3(ctx, field, ncomp, ncomp), d3 = grid_to3(ctx, disp, 2, 3);
+      upload_f32(e, f3.data(), ncomp * N, f.p);
+      upload_f32(e, d3.data(), 3 * N, d.p);
+    } else {
+      upload_f32(e, field, ncomp * N, f.p);
+      upload_f32(e, disp, 3 * N, d.p);
+    }
     if (kind == LDDMM_INTERP_CUBIC)
       e.warp_grid(f.p, ncomp, d.p, o.p);
     else
       e.warp_nearest(f.p, ncomp, d.p, o.p);
-    download_f64(e, o.p, ncomp * N, out);
+    fetch_grid(ctx, o.p, ncomp, out);
   });
 }
 
@@ -528,10 +663,15 @@ int lddmm_jacobian(lddmm_ctx* ctx, const double* disp, double* det, double minma
     Engine& e = *ctx->eng;
     const long long N = e.npts();
     DevBuf<float> d(3 * N);
-    upload_f32(e, disp, 3 * N, d.p);
+    if (ctx->d == 2) {
+      const std::vector<double> d3 = grid_to3(ctx, disp, 2, 3);
+      upload_f32(e, d3.data(), 3 * N, d.p);
+    } else {
+      upload_f32(e, disp, 3 * N, d.p);
+    }
     DevBuf<float> o(det ? N : 1);
     e.jacobian_grid(d.p, det ? o.p : nullptr, minmax);
-    if (det) download_f64(e, o.p, N, det);
+    if (det) fetch_grid(ctx, o.p, 1, det);
   });
 }
 
@@ -540,8 +680,15 @@ int lddmm_mean_dice(lddmm_ctx* ctx, const double* a, const double* b, double* ou
     Engine& e = *ctx->eng;
     const long long N = e.npts();
     DevBuf<float> da(N), db(N);
-    upload_f32(e, a, N, da.p);
-    upload_f32(e, b, N, db.p);
+    if (ctx->d == 2) {
+      // Dice of the z-replicated labels = Dice of the 2-D labels (every count times zr)
+      const std::vector<double> a3 = grid_to3(ctx, a, 1, 1), b3 = grid_to3(ctx, b, 1, 1);
+      upload_f32(e, a3.data(), N, da.p);
+      upload_f32(e, b3.data(), N, db.p);
+    } else {
+      upload_f32(e, a, N, da.p);
+      upload_f32(e, b, N, db.p);
+    }
     *out = mean_dice_dev(e, da.p, db.p);
   });
 }
@@ -551,7 +698,12 @@ int lddmm_vel_from_spatial(lddmm_ctx* ctx, const double* host_vec, double* v) {
     Engine& e = *ctx->eng;
     const long long N = e.npts(), V = e.vec_elems();
     DevBuf<float> g(3 * N);
-    upload_f32(e, host_vec, 3 * N, g.p);
+    if (ctx->d == 2) {
+      const std::vector<double> g3 = grid_to3(ctx, host_vec, 2, 3);
+      upload_f32(e, g3.data(), 3 * N, g.p);
+    } else {
+      upload_f32(e, host_vec, 3 * N, g.p);
+    }
     e.project(g.p, 3, D2(v));
     const int nodes = (int)(e.vel_elems() / V);
     for (int i = 1; i < nodes; ++i)
@@ -568,7 +720,7 @@ int lddmm_vel_to_spatial(lddmm_ctx* ctx, const double* v, int node, double* host
     shape_require(node >= 0 && node < nodes, "lddmm_vel_to_spatial: node out of range");
     DevBuf<float> g(3 * N);
     e.embed(D2(v) + node * V, 3, g.p, false);
-    download_f64(e, g.p, 3 * N, host_vec);
+    fetch_grid(ctx, g.p, ctx->d, host_vec);
   });
 }
 

@@ -8,9 +8,8 @@
 // warps, Jacobians and Dice counts run on the GPU through liblddmm_cuda.so;
 // this file only parses arguments, reads/writes files and formats reports.
 //
-// Scope: the band representation on 3-D grids, SL-RK2 or RK4 transport.
-// --repr spatial and 2-D registrations exit with status 1 and say so
-// (SURVEY.md §8f4).  `synth` generates 2-D and 3-D blobs/discs fixtures with
+// Scope: the band representation on 2-D and 3-D grids, SL-RK2 or RK4 transport.
+// --repr spatial exits with status 1 and says so.  `synth` generates 2-D and 3-D blobs/discs fixtures with
 // the reference's seeded generators (synth.hpp:20-42,182-259) restated here.
 #include <algorithm>
 #include <array>
@@ -270,18 +269,18 @@ struct Ctx {
   }
 };
 
-void require_3d(const Grid& g) {
-  if (g.d != 3) throw InputError("the B200 engine registers 3-D grids only (got d = " + std::to_string(g.d) + ")");
+void require_2d_or_3d(const Grid& g) {
+  if (g.d != 2 && g.d != 3) throw InputError("grid dimension must be 2 or 3 (got d = " + std::to_string(g.d) + ")");
 }
 
 lddmm_problem problem_for(const Grid& g, int band, int nt, int variant, int param, double alpha, int s,
                           double sigma2) {
   lddmm_problem p{};
-  p.d = 3;
+  p.d = g.d;  // 2-D grids run z-replicated inside the engine (lddmm_cuda.h)
   for (int a = 0; a < 3; ++a) {
-    p.dims[a] = g.dims[a];
-    p.spacing[a] = g.spacing[a];
-    p.band[a] = std::min(band, g.dims[a]);  // lddmm_cli.cpp:222-224
+    p.dims[a] = a < g.d ? g.dims[a] : 1;
+    p.spacing[a] = a < g.d ? g.spacing[a] : 1.0;
+    p.band[a] = a < g.d ? std::min(band, g.dims[a]) : 1;  // lddmm_cli.cpp:222-224
   }
   p.nt = nt;
   p.variant = variant;
@@ -363,7 +362,7 @@ int do_register(const RegOpts& o) {
   if (o.repr == "spatial")
     throw InputError("--repr spatial is not part of the B200 engine (band representation only)");
   if (!(o.band >= 4 && o.band % 2 == 0)) throw InputError("--band must be even and >= 4");
-  require_3d(I0.grid);
+  require_2d_or_3d(I0.grid);
   const Grid& g = I0.grid;
   const std::size_t N = g.size();
 
@@ -395,8 +394,8 @@ int do_register(const RegOpts& o) {
   hist.resize((std::size_t)res.n_history);
 
   // compute_maps, warp(I0, forward_pts, cubic), Jacobian ranges (metrics.hpp:24-79)
-  Field fwd{g, Kind::vector, 3, std::vector<double>(3 * N)};
-  Field inv{g, Kind::vector, 3, std::vector<double>(3 * N)};
+  Field fwd{g, Kind::vector, g.d, std::vector<double>(g.d * N)};
+  Field inv{g, Kind::vector, g.d, std::vector<double>(g.d * N)};
   double jac[4];
   ctx.check(lddmm_maps(ctx.h, v, fwd.v.data(), inv.v.data(), jac));
   Field warped{g, Kind::scalar, 1, std::vector<double>(N)};
@@ -407,7 +406,7 @@ int do_register(const RegOpts& o) {
   write_field(join_path(o.out, "warped_source"), warped);
   const int nodes = param == LDDMM_STATIONARY ? 1 : nt + 1;
   for (int i = 0; i < nodes; ++i) {
-    Field vel{g, Kind::vector, 3, std::vector<double>(3 * N)};
+    Field vel{g, Kind::vector, g.d, std::vector<double>(g.d * N)};
     ctx.check(lddmm_vel_to_spatial(ctx.h, v, i, vel.v.data()));
     if (param == LDDMM_STATIONARY) {
       write_field(join_path(o.out, "velocity"), vel);
@@ -518,7 +517,7 @@ int do_evaluate(const EvalOpts& o) {
   rep["mse_rel"] = mse_rel(warped, tgt, src);
   const bool want_dice = !o.warped_labels.empty() && !o.target_labels.empty();
   if (want_dice || !o.displacement.empty()) {
-    require_3d(tgt.grid);
+    require_2d_or_3d(tgt.grid);
     // an engine context on this grid (the smallest band; only grid buffers are used)
     Ctx ctx(problem_for(tgt.grid, 4, 1, LDDMM_DEFORMATION_STATE_EQUATION, LDDMM_STATIONARY, 0.0025, 2, 1.0));
     if (want_dice) {

@@ -555,7 +555,7 @@ void Engine::provider_build(const double2* v, ProviderState& ps, bool with_bwd) 
   sync();
   double vmax = 0.0;
   for (int i = 0; i < nn; ++i) vmax = std::max(vmax, host_slots_[16 + i]);
-  const double hmin = std::min(h_[0], std::min(h_[1], h_[2]));
+  const double hmin = prob_.d == 2 ? std::min(h_[0], h_[1]) : std::min(h_[0], std::min(h_[1], h_[2]));
   ps.cfl = vmax * dt / hmin;
 }
 
@@ -872,7 +872,7 @@ double Engine::tv_inner(const double2* a, const double2* b) {  // variants.hpp:9
 }
 double Engine::tv_linf(const double2* a) {
   const int g = launch_linf_partial(vel_elems(), a, part_.p, stream_);
-  return reduce(g, 1);
+  return reduce(g, 1) / prob_.zrep;  // 2-D: the 2-D coefficients' max norm
 }
 bool Engine::tv_all_finite(const double2* a) {
   const int g = launch_nonfinite_partial(vel_elems(), a, part_.p, stream_);

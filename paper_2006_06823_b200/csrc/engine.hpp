@@ -26,6 +26,14 @@ struct Problem {
   double alpha = 0.0025;
   int s = 2;
   double sigma2 = 1.0;
+  // 2-D problems (core.hpp:49-52 allows d = 2) run as 3-D problems with the z axis
+  // replicated zrep times at spacing 1/zrep: every field is z-constant, only the kz = 0
+  // band plane is non-zero, and all reference quantities (inner products, energies,
+  // Jacobians) are exactly the 2-D ones; d sets which axes enter h_min (cfl) and
+  // zrep rescales the band coefficients' max norm (the 3-D coefficients are zrep times
+  // the 2-D ones).
+  int d = 3;
+  int zrep = 1;
 };
 
 struct Energies {

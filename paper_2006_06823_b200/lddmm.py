@@ -98,6 +98,8 @@ def lib():
             "lddmm_vel_axpy": [vp, C.c_double, vp, vp, vp],
             "lddmm_vel_scale": [vp, vp, C.c_double, vp],
             "lddmm_vel_inner": [vp, vp, vp, C.POINTER(C.c_double)],
+            "lddmm_vel_upload": [vp, vp, vp],
+            "lddmm_vel_download": [vp, vp, vp],
             "lddmm_vel_linf": [vp, vp, C.POINTER(C.c_double)],
             "lddmm_vel_all_finite": [vp, vp, C.POINTER(C.c_int)],
             "lddmm_forward": [vp, vp, C.c_int, C.POINTER(_Energies), C.POINTER(C.c_int)],
@@ -260,14 +262,14 @@ class Context:
                  lop: SobolevOperator = None, parameterization="stationary", device=0, integrator="sl"):
         lop = lop or SobolevOperator()
         g = band.parent
-        if g.d != 3:
-            raise ShapeError("the CUDA engine supports 3-D grids")
+        if g.d not in (2, 3):
+            raise ShapeError("grid dimension must be 2 or 3 (core.hpp:49-52)")
         p = _Problem()
-        p.d = 3
+        p.d = g.d
         for a in range(3):
-            p.dims[a] = g.dims[a]
-            p.spacing[a] = float(g.spacing[a])
-            p.band[a] = band.bounds[a]
+            p.dims[a] = g.dims[a] if a < g.d else 1
+            p.spacing[a] = float(g.spacing[a]) if a < g.d else 1.0
+            p.band[a] = band.bounds[a] if a < g.d else 1
         p.nt = nt
         p.variant = VARIANTS[variant]
         p.parameterization = 0 if parameterization == "stationary" else 1
@@ -302,7 +304,16 @@ class Context:
 
     @property
     def vel_shape(self):
-        return (self.nodes, 3) + tuple(self.band.bounds)
+        """Host layout of a velocity (the reference's BandVectorField per node)."""
+        return (self.nodes, self.grid.d) + tuple(self.band.bounds)
+
+    @property
+    def dev_vel_shape(self):
+        """Device layout: 3-D; a 2-D problem runs with its z axis replicated (Problem::zrep),
+        only the kz = 0 plane of the x, y components non-zero, scaled by the replica count."""
+        if self.grid.d == 3:
+            return self.vel_shape
+        return (self.nodes, 3) + tuple(self.band.bounds) + (4,)
 
     def stream_ptr(self):
         return int(lib().lddmm_stream(self.h))
@@ -336,12 +347,14 @@ def _raise(rc, msg, step=-1):
 class Velocity:
     """TimeVaryingVelocity<BandVectorField> (core.hpp:275-317) resident on the device.
 
-    Storage: torch float64 CUDA tensor [nodes, 3, Kx, Ky, Kz, 2] (interleaved re/im)."""
+    Storage: torch float64 CUDA tensor [nodes, 3, Kx, Ky, Kz, 2] (interleaved re/im); a 2-D
+    problem keeps the engine's internal 3-D layout on the device (Context.dev_vel_shape) and
+    converts through lddmm_vel_upload / lddmm_vel_download."""
 
     def __init__(self, ctx: Context, data=None):
         torch = _torch()
         self.ctx = ctx
-        self.t = torch.zeros(ctx.vel_shape + (2,), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        self.t = torch.zeros(ctx.dev_vel_shape + (2,), dtype=torch.float64, device=f"cuda:{ctx.device}")
         if data is not None:
             self.set(data)
 
@@ -350,6 +363,15 @@ class Velocity:
 
     def set(self, data):
         torch = _torch()
+        if self.ctx.grid.d == 2:
+            if isinstance(data, torch.Tensor):
+                data = data.detach().cpu().numpy()
+                if not np.iscomplexobj(data):
+                    data = data.view(np.complex128)
+            a = np.ascontiguousarray(np.asarray(data, dtype=np.complex128).reshape(self.ctx.vel_shape))
+            torch.cuda.synchronize(self.ctx.device)
+            self.ctx.check(lib().lddmm_vel_upload(self.ctx.h, self.ptr(), a.ctypes.data_as(C.c_void_p)))
+            return self
         if isinstance(data, torch.Tensor):
             if data.is_complex():
                 data = torch.view_as_real(data)
@@ -362,6 +384,10 @@ class Velocity:
     def numpy(self):
         torch = _torch()
         torch.cuda.synchronize(self.ctx.device)
+        if self.ctx.grid.d == 2:
+            out = np.zeros(self.ctx.vel_shape, dtype=np.complex128)
+            self.ctx.check(lib().lddmm_vel_download(self.ctx.h, self.ptr(), out.ctypes.data_as(C.c_void_p)))
+            return out
         return self.t.cpu().numpy().view(np.complex128).reshape(self.ctx.vel_shape)
 
     def copy(self):
@@ -459,7 +485,7 @@ class Model:
         return out.reshape(self.grid.dims)
 
     def series(self, which="u"):
-        shape = (self.nt + 1, 3) + tuple(self.band.bounds)
+        shape = (self.nt + 1, self.grid.d) + tuple(self.band.bounds)
         out = np.zeros(int(np.prod(shape)) * 2)
         self.ctx.check(lib().lddmm_get_series(self.ctx.h, 0 if which == "u" else 1, out.ctypes.data_as(C.c_void_p)))
         return out.view(np.complex128).reshape(shape)
@@ -531,13 +557,13 @@ def maps_jacobian(ctx: Context, v_host):
 def compute_maps(model: Model, v: Velocity):
     """compute_maps + map_jacobian_determinant ranges (metrics.hpp:24-79).
     Returns (forward_disp, inverse_disp, jac) with jac = [fmin, fmax, imin, imax]."""
-    n = 3 * model.grid.size()
+    n = model.grid.d * model.grid.size()
     f = np.zeros(n)
     i = np.zeros(n)
     jac = (C.c_double * 4)()
     model.ctx.check(lib().lddmm_maps(model.ctx.h, v.ptr(), f.ctypes.data_as(C.c_void_p),
                                      i.ctypes.data_as(C.c_void_p), jac))
-    shape = (3,) + tuple(model.grid.dims)
+    shape = (model.grid.d,) + tuple(model.grid.dims)
     return f.reshape(shape), i.reshape(shape), np.array(list(jac))
 
 
@@ -553,9 +579,9 @@ def _f64(a):
 
 def warp(ctx: Context, field, disp, kind="cubic"):
     """warp(f, x - disp, cubic) / warp_nearest(f, x - disp) (interp.hpp:178-225); field
-    [N...] or [C, N...], disp [3, N...] in physical units; fp32 on the device."""
+    [N...] or [C, N...], disp [d, N...] in physical units; fp32 on the device."""
     f = _f64(field)
-    nc = 1 if f.ndim == 3 else f.shape[0]
+    nc = 1 if f.ndim == ctx.grid.d else f.shape[0]
     out = np.zeros_like(f)
     d = _f64(disp)
     ctx.check(lib().lddmm_warp(ctx.h, INTERP[kind], f.ctypes.data_as(C.c_void_p), nc, d.ctypes.data_as(C.c_void_p),
@@ -600,8 +626,8 @@ def velocity_from_spatial(model: "Model", field) -> "Velocity":
 
 
 def velocity_to_spatial(model: "Model", v: "Velocity", node=0):
-    """Alg::to_spatial (embed) of one velocity node -> [3, N...] grid field."""
-    out = np.zeros((3,) + tuple(model.grid.dims))
+    """Alg::to_spatial (embed) of one velocity node -> [d, N...] grid field."""
+    out = np.zeros((model.grid.d,) + tuple(model.grid.dims))
     model.ctx.check(lib().lddmm_vel_to_spatial(model.ctx.h, v.ptr(), int(node), out.ctypes.data_as(C.c_void_p)))
     return out
 
