@@ -55,8 +55,12 @@ typedef struct lddmm_ctx lddmm_ctx;
 /* Model<BandAlgebra> construction data: GridSpec (core.hpp:42-122), BandSpec
  * (spectral.hpp:22-83), Model fields variant/nt/sigma2/lop (variants.hpp:237-244),
  * SobolevOperator (spectral.hpp:518-525), Model::integrator (variants.hpp:241).
- * d = 3, band representation; SL-RK2 (default) or RK4 transport; all three
- * variants; stationary and nonstationary. */
+ * d = 3 or 2, band representation; SL-RK2 (default) or RK4 transport; all three
+ * variants; stationary and nonstationary.  d = 2: dims/spacing/band[2] are ignored;
+ * every host-side layout of the ABI (images, fields, displacements, band velocities,
+ * series) is the reference's 2-D one (2 vector components, Kx x Ky band); the engine
+ * runs the problem z-replicated internally, so device velocity buffers and the
+ * lddmm_op_* primitives use the internal 3-D layout. */
 typedef struct {
   int d;
   int dims[3];

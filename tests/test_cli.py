@@ -65,14 +65,11 @@ def test_usage_and_input_errors(tmp_path):
     r = run("register", "--source", str(tmp_path / "nope.raw"), "--target", str(tmp_path / "nope.raw"),
             "--out", str(tmp_path / "o"))
     assert r.returncode == 1 and "cannot open sidecar" in r.stderr
-    # 2-D inputs and the spatial representation are outside the engine: status 1 with a reason
+    # the spatial representation is outside the engine: status 1 with a reason
     assert run("synth", "--kind", "blobs", "--n", "16", "--out", str(tmp_path / "b2")).returncode == 0
     r = run("register", "--source", str(tmp_path / "b2" / "source.raw"), "--target",
-            str(tmp_path / "b2" / "target.raw"), "--out", str(tmp_path / "o2"))
-    assert r.returncode == 1 and "3-D" in r.stderr
-    r = run("register", "--source", str(tmp_path / "b2" / "source.raw"), "--target",
             str(tmp_path / "b2" / "target.raw"), "--out", str(tmp_path / "o3"), "--repr", "spatial")
-    assert r.returncode == 1
+    assert r.returncode == 1 and "spatial" in r.stderr
     # payload / sidecar mismatch (io.hpp:66-80)
     with open(tmp_path / "b2" / "source.raw", "ab") as f:
         f.write(b"\0\0\0\0")

@@ -190,3 +190,37 @@ def test_two_disc_dice_matches_reference(cuda, seed):
         fwd, _, _ = L.compute_maps(m, res.v)
         d = L.mean_dice(ctx, L.warp(ctx, sl, fwd, kind="nearest"), tl)
         assert abs(d - float(z[f"s{seed}_{v}_dice"])) < 5e-3
+
+
+def test_cli_register_2d_matches_reference(cuda, tmp_path):
+    """`lddmm register` on a 2-D two-disc fixture (the reference CLI's default use) against
+    the reference library run on the same rescaled images: GN path, final energy, mse_rel,
+    Jacobian ranges, and the 2-D output layouts."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    r = run("synth", "--kind", "discs", "--d", "2", "--n", "64", "--seed", "5", "--out", str(tmp_path / "d"))
+    assert r.returncode == 0, r.stderr
+    d, out = tmp_path / "d", tmp_path / "reg"
+    r = run("register", "--source", str(d / "source.raw"), "--target", str(d / "target.raw"),
+            "--source-labels", str(d / "source_labels.raw"), "--target-labels", str(d / "target_labels.raw"),
+            "--out", str(out), "--variant", "deformation_state_equation", "--band", "16", "--sigma2", "0.01",
+            "--max-iter", "6")
+    assert r.returncode == 0, r.stderr
+    with open(out / "report.json") as f:
+        rep = json.load(f)
+    _, src = read_field(str(d / "source"))
+    _, tgt = read_field(str(d / "target"))
+    dims = src.shape
+    s = ref.rescale_unit(src.astype(np.float64), dims, (1.0, 1.0))
+    t = ref.rescale_unit(tgt.astype(np.float64), dims, (1.0, 1.0))
+    m = ref.RefModel(s, t, dims, (1.0, 1.0), (16, 16), "deformation_state_equation", 5, 0.01)
+    want = m.optimize(None, max_iter=6, pcg_max_iter=5)
+    _, _, jac = m.maps(want["v"])
+    assert rep["stop_reason"] == want["stop"] and rep["iterations"] == want["iterations"]
+    assert abs(rep["final_energy"] - want["history"][-1].energy) <= 1e-5 * abs(want["history"][-1].energy)
+    assert abs(rep["mse_rel_final"] - want["history"][-1].mse_rel) <= 1e-5
+    assert np.allclose([rep["jacobian_forward"]["min"], rep["jacobian_forward"]["max"],
+                        rep["jacobian_inverse"]["min"], rep["jacobian_inverse"]["max"]], jac, atol=1e-4)
+    side, fwd = read_field(str(out / "displacement_forward"))
+    assert side["components"] == 2 and fwd.shape == (2,) + dims
