@@ -557,6 +557,8 @@ void Engine::provider_build(const double2* v, ProviderState& ps, bool with_bwd) 
   for (int i = 0; i < nn; ++i) vmax = std::max(vmax, host_slots_[16 + i]);
   const double hmin = prob_.d == 2 ? std::min(h_[0], h_[1]) : std::min(h_[0], std::min(h_[1], h_[2]));
   ps.cfl = vmax * dt / hmin;
+  // whole-map pull-backs of this forward move nodes by up to max|v| T / h = cfl nt voxels
+  pullback_large_ = ps.cfl * prob_.nt > 1.0;
 }
 
 void Engine::departure(const double2* v, float* dep_fwd, float* dep_bwd, double* cfl) {
@@ -703,7 +705,7 @@ void Engine::solve_incremental_displacement(ProviderState& ps, const double2* dv
 void Engine::warp_m1(const double2* u1, float* m1, float* res, bool want_gsw, double* data_sumsq) {
   const long long N = npts();
   embed(u1, 3, ugrid_.p, false);
-  launch_warp_by_displacement(I0coef_.p, want_gsw ? 4 : 1, ugrid_.p, h_, m1, full_.N, stream_);
+  launch_warp_by_displacement(I0coef_.p, want_gsw ? 4 : 1, ugrid_.p, h_, m1, full_.N, stream_, pullback_large_);
   const int g = launch_residual(N, m1, I1_.p, res, part_.p, stream_);
   *data_sumsq = reduce(g, 0);
 }

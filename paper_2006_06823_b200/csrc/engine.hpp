@@ -318,6 +318,7 @@ class Engine {
   void timed_gather(const float* coef, int ncomp, const float* dep, float* out);
 
   int gt_on_ = 0;
+  bool pullback_large_ = false;  // set by provider_build: whole-map pull-backs exceed a voxel
   std::vector<cudaEvent_t> gt_events_;
   std::vector<double> gt_bytes_;
   std::vector<int> gt_kind_;

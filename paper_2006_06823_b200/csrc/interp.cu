@@ -64,7 +64,8 @@ __device__ __forceinline__ void sample(const float* __restrict__ coef, long long
 template <int F>
 __global__ __launch_bounds__(256) void gather_cubic_kernel(const float* __restrict__ coef,
                                                            const float* __restrict__ disp,
-                                                           float* __restrict__ out, int Nx, int Ny, int Nz) {
+                                                           float* __restrict__ out, int Nx, int Ny, int Nz,
+                                                           float3 sc) {
   const long long N = (long long)Nx * Ny * Nz;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N;
        p += (long long)gridDim.x * blockDim.x) {
@@ -73,7 +74,8 @@ __global__ __launch_bounds__(256) void gather_cubic_kernel(const float* __restri
     const int j = (int)(q % Ny);
     const int i = (int)(q / Ny);
     Stencil s;
-    make_stencil(i, j, k, __ldg(disp + p), __ldg(disp + N + p), __ldg(disp + 2 * N + p), Nx, Ny, Nz, s);
+    make_stencil(i, j, k, sc.x * __ldg(disp + p), sc.y * __ldg(disp + N + p), sc.z * __ldg(disp + 2 * N + p), Nx,
+                 Ny, Nz, s);
     float v[F];
     sample<F>(coef, N, Ny, Nz, s, v);
 #pragma unroll
@@ -727,8 +729,8 @@ void launch_gather_cubic_tiled(const float* coef, int ncomp, const float* disp, 
   }
 }
 
-void launch_gather_cubic_global(const float* coef, int ncomp, const float* disp, float* out, const int* N,
-                                cudaStream_t s) {
+static void launch_gather_global_scaled(const float* coef, int ncomp, const float* disp, float* out, const int* N,
+                                       float3 sc, cudaStream_t s) {
   const long long n = (long long)N[0] * N[1] * N[2];
   const int grid = grid_for(n, 256, 16);
   int done = 0;
@@ -737,17 +739,25 @@ void launch_gather_cubic_global(const float* coef, int ncomp, const float* disp,
     const float* c = coef + (long long)done * n;
     float* o = out + (long long)done * n;
     if (left >= 6) {
-      gather_cubic_kernel<6><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2]);
+      gather_cubic_kernel<6><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
       done += 6;
+    } else if (left >= 4) {
+      gather_cubic_kernel<4><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
+      done += 4;
     } else if (left >= 3) {
-      gather_cubic_kernel<3><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2]);
+      gather_cubic_kernel<3><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
       done += 3;
     } else {
-      gather_cubic_kernel<1><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2]);
+      gather_cubic_kernel<1><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
       done += 1;
     }
     LDDMM_LAUNCH_CHECK();
   }
+}
+
+void launch_gather_cubic_global(const float* coef, int ncomp, const float* disp, float* out, const int* N,
+                                cudaStream_t s) {
+  launch_gather_global_scaled(coef, ncomp, disp, out, N, make_float3(1.f, 1.f, 1.f), s);
 }
 
 // ---------------------------------------------------------------------------
@@ -811,11 +821,20 @@ void launch_departure(const float* vgrid, const float* vcoef, double dt, const d
 }
 
 // pull-back through points x - disp (disp physical): the production gather with
-// displacement scale -1/h (m1 = I0 o phi1, grad_src_warped, warp of grid fields)
+// displacement scale -1/h (m1 = I0 o phi1, grad_src_warped, warp of grid fields).
+// `large`: the caller expects multi-voxel displacements (a whole deformation map, e.g.
+// u(1) with max |v| T / h > 1): most nodes leave the window regime, and the plain
+// per-node gather (L1 / L2 taps, weights shared by the components) beats the staged
+// window kernel with its per-node fallback (2.3x at 1.5 voxels, 3.6x at 4,
+// tools/lab/gather_lab.py); both are bitwise the same samples.
 void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp_phys, const double* h,
-                                 float* out, const int* N, cudaStream_t s) {
-  launch_gather_scaled(coef, ncomp, disp_phys, -(float)(1.0 / h[0]), -(float)(1.0 / h[1]), -(float)(1.0 / h[2]),
-                       out, N, s, false);
+                                 float* out, const int* N, cudaStream_t s, bool large) {
+  const float3 sc = make_float3(-(float)(1.0 / h[0]), -(float)(1.0 / h[1]), -(float)(1.0 / h[2]));
+  if (large) {
+    launch_gather_global_scaled(coef, ncomp, disp_phys, out, N, sc, s);
+    return;
+  }
+  launch_gather_scaled(coef, ncomp, disp_phys, sc.x, sc.y, sc.z, out, N, s, false);
 }
 
 // ---------------------------------------------------------------------------

@@ -120,7 +120,7 @@ void launch_gather_scaled(const float* coef, int ncomp, const float* disp, float
 // cubic pull-back of coef at x - disp_phys where disp is a grid field in physical units
 // (points_from_displacement, variants.hpp:49-51); out[c] for ncomp coefficient fields
 void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp_phys, const double* h,
-                                 float* out, const int* N, cudaStream_t s);
+                                 float* out, const int* N, cudaStream_t s, bool large = false);
 // nearest-neighbour pull-back (warp_nearest, interp.hpp:213-225): out[c](x) =
 // f[c](wrap(llround((x - disp(x)) / h))), fp64 index arithmetic
 void launch_warp_nearest(const float* f, int ncomp, const float* disp_phys, const double* h, float* out,

@@ -236,7 +236,8 @@ void Engine::lambda_nodes_state(const float* lam1, double2* out_series) {
   const int nt = prob_.nt;
   grid_spline(lam1, lcoef_.p);
   for (int i = 0; i <= nt; ++i) {
-    launch_warp_by_displacement(lcoef_.p, 1, psi_f_.p + i * 3 * N, h_, gridB_.p, full_.N, stream_);
+    launch_warp_by_displacement(lcoef_.p, 1, psi_f_.p + i * 3 * N, h_, gridB_.p, full_.N, stream_,
+                                pullback_large_);
     launch_mul_f32(N, jac_f_.p + i * N, gridB_.p, gridB_.p, stream_);
     project(gridB_.p, 1, out_series + i * S);
   }
@@ -281,11 +282,11 @@ double Engine::forward_state(bool with_adjoint) {
   warp_m1(u_.p + nt * V, m1_.p, res_.p, false, &ss);
   if (!with_adjoint) return ss;
   // grad_src_warped from the band-filtered gradient (variants.hpp:176-178,421); ugrid_ = iota(u(1))
-  launch_warp_by_displacement(fgI0coef_.p, 3, ugrid_.p, h_, m1_.p + N, full_.N, stream_);
+  launch_warp_by_displacement(fgI0coef_.p, 3, ugrid_.p, h_, m1_.p + N, full_.N, stream_, pullback_large_);
   // image reconstructions m_i = pi(I0 o (x - iota(u_i)))
   for (int i = 0; i <= nt; ++i) {
     embed(u_.p + i * V, 3, ugrid_.p, false);
-    launch_warp_by_displacement(I0coef_.p, 1, ugrid_.p, h_, gridB_.p, full_.N, stream_);
+    launch_warp_by_displacement(I0coef_.p, 1, ugrid_.p, h_, gridB_.p, full_.N, stream_, pullback_large_);
     project(gridB_.p, 1, m_ser_.p + i * S);
   }
   solve_displacement(prov_, false, nu_ser_.p);

@@ -47,7 +47,7 @@ if real:
 ref = {nc: ops.gather(coef[:nc].contiguous(), dep, 2) for nc in (1, 3, 6)}
 flush = torch.empty(512 * 1024 * 1024 // 4, device="cuda")
 stream = torch.cuda.ExternalStream(ctx.stream_ptr())  # events on the engine stream the kernels run on
-for impl in (0, 4, 3):
+for impl in tuple(int(x) for x in os.environ.get("GATHER_LAB_IMPLS", "0,4,3").split(",")):
     for nc in (3, 6, 1):
         c = coef[:nc].contiguous()
         try:
