@@ -684,10 +684,37 @@ void Engine::solve_incremental_displacement(ProviderState& ps, const double2* dv
   const long long V = vec_elems(), K = kprod();
   const int nt = prob_.nt;
   const double dt = 1.0 / nt;
-  // sources src_i = -jac(u_i, dv_i) + dv_i ; u_0 = 0 so src_0 = dv_0 exactly
+  // sources src_i = -jac(u_i, dv_i) + dv_i ; u_0 = 0 so src_0 = dv_0 exactly.  The
+  // sources do not depend on du, so the nodes go through the small grid in batches (one
+  // embed / product / project pipeline per batch instead of per node; every field takes
+  // the same arithmetic as in a single small_product, so the values are identical)
   LDDMM_CUDA(cudaMemcpyAsync(src_.p, dv, V * sizeof(double2), cudaMemcpyDeviceToDevice, stream_));
-  for (int i = 1; i <= nt; ++i)
-    small_product(3, u_.p + i * V, tvnode(dv, i), src_.p + i * V, -1.0, tvnode(dv, i), 1.0);
+  {
+    const long long M = small_.npts();
+    const bool stat = prob_.stationary != 0;
+    const int per = stat ? std::min((fmax_small_ - 3) / 9, 6) : std::min(fmax_small_ / 12, 5);
+    for (int i0 = 1; i0 <= nt; i0 += per) {
+      const int nn = std::min(per, nt + 1 - i0);
+      PrepArgs pa{};
+      for (int n = 0; n < nn; ++n)
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b)
+            pa.f[n * 9 + a * 3 + b] = PrepField{u_.p + (i0 + n) * V + a * K, SYM_DERIV_X + b, 1.0};
+      const int nw = stat ? 1 : nn;  // dv fields: one set (stationary) or one per node
+      for (int n = 0; n < nw; ++n)
+        for (int c = 0; c < 3; ++c) pa.f[9 * nn + n * 3 + c] = PrepField{tvnode(dv, i0 + n) + c * K, SYM_NONE, 1.0};
+      pa.nf = 9 * nn + 3 * nw;
+      embed_fields(small_, pa, sgrid_.p, sD_.p, sE1_.p, sE2_.p);
+      launch_jac_batch(false, nn, M, sgrid_.p, sgrid_.p + 9 * nn * M, stat ? 0 : 3 * M, sacc_.p, 3 * M,
+                       NodeWeights{}, true, stream_);
+      FinArgs fa{};
+      fa.nf = 3 * nn;
+      for (int n = 0; n < nn; ++n)
+        for (int c = 0; c < 3; ++c)
+          fa.f[n * 3 + c] = FinField{src_.p + (i0 + n) * V + c * K, -small_ratio_, tvnode(dv, i0 + n) + c * K, 1.0};
+      project_fields(small_, sacc_.p, fa, sG1_.p, sG2_.p, sG3_.p);
+    }
+  }
   LDDMM_CUDA(cudaMemsetAsync(series, 0, V * sizeof(double2), stream_));
   for (int s = 0; s < nt; ++s) {
     double2* in = bt(0);
