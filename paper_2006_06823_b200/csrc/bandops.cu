@@ -14,6 +14,7 @@ namespace lddmm_b200 {
 
 __global__ void axpby_kernel(long long n, double a, const double2* __restrict__ x, double b,
                              const double2* __restrict__ y, double2* __restrict__ out) {
+  pdl_prologue();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double2 xv = x[i];
     double2 r;
@@ -33,16 +34,16 @@ __global__ void axpby_kernel(long long n, double a, const double2* __restrict__ 
 }
 
 void launch_axpy(long long n, double a, const double2* x, const double2* y, double2* out, cudaStream_t s) {
-  axpby_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, x, 1.0, y, out);
+  pdl_launch(axpby_kernel, grid_for(n, 256, 4), 256, 0, s, n, a, x, 1.0, y, out);
   LDDMM_LAUNCH_CHECK();
 }
 void launch_axpby(long long n, double a, const double2* x, double b, const double2* y, double2* out,
                   cudaStream_t s) {
-  axpby_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, x, b, y, out);
+  pdl_launch(axpby_kernel, grid_for(n, 256, 4), 256, 0, s, n, a, x, b, y, out);
   LDDMM_LAUNCH_CHECK();
 }
 void launch_scale(long long n, double a, const double2* x, double2* out, cudaStream_t s) {
-  axpby_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, x, 0.0, nullptr, out);
+  pdl_launch(axpby_kernel, grid_for(n, 256, 4), 256, 0, s, n, a, x, 0.0, nullptr, out);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -51,6 +52,7 @@ __device__ __forceinline__ int signed_freq(int f, int K) { return f < K / 2 ? f 
 __global__ void sobolev_kernel(const double2* __restrict__ in, double2* __restrict__ out, int ncomp, int Kx,
                                int Ky, int Kz, double wx, double wy, double wz, double alpha, double s,
                                int inverse) {
+  pdl_prologue();
   const long long per = (long long)Kx * Ky * Kz;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per; i += (long long)gridDim.x * blockDim.x) {
     const int fz = (int)(i % Kz);
@@ -73,13 +75,14 @@ __global__ void sobolev_kernel(const double2* __restrict__ in, double2* __restri
 void launch_sobolev(const double2* in, double2* out, int ncomp, const int* K, const double* wunit, double alpha,
                     int s, bool inverse, cudaStream_t st) {
   const long long per = (long long)K[0] * K[1] * K[2];
-  sobolev_kernel<<<grid_for(per, 256, 4), 256, 0, st>>>(in, out, ncomp, K[0], K[1], K[2], wunit[0], wunit[1],
+  pdl_launch(sobolev_kernel, grid_for(per, 256, 4), 256, 0, st, in, out, ncomp, K[0], K[1], K[2], wunit[0], wunit[1],
                                                          wunit[2], alpha, (double)s, inverse ? 1 : 0);
   LDDMM_LAUNCH_CHECK();
 }
 
 __global__ void divergence_kernel(const double2* __restrict__ v, double2* __restrict__ out, int Kx, int Ky, int Kz,
                                   double wx, double wy, double wz) {
+  pdl_prologue();
   const long long per = (long long)Kx * Ky * Kz;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per; i += (long long)gridDim.x * blockDim.x) {
     const int fz = (int)(i % Kz);
@@ -99,7 +102,7 @@ __global__ void divergence_kernel(const double2* __restrict__ v, double2* __rest
 
 void launch_band_divergence(const double2* v, double2* out, const int* K, const double* wunit, cudaStream_t s) {
   const long long per = (long long)K[0] * K[1] * K[2];
-  divergence_kernel<<<grid_for(per, 256, 4), 256, 0, s>>>(v, out, K[0], K[1], K[2], wunit[0], wunit[1], wunit[2]);
+  pdl_launch(divergence_kernel, grid_for(per, 256, 4), 256, 0, s, v, out, K[0], K[1], K[2], wunit[0], wunit[1], wunit[2]);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -107,6 +110,7 @@ void launch_band_divergence(const double2* v, double2* out, const int* K, const 
 
 __global__ __launch_bounds__(256) void inner_partial_kernel(long long n, const double2* __restrict__ x,
                                                             const double2* __restrict__ y, double* part) {
+  pdl_prologue();
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double2 a = x[i], b = y[i];
@@ -117,6 +121,7 @@ __global__ __launch_bounds__(256) void inner_partial_kernel(long long n, const d
 }
 
 __global__ __launch_bounds__(256) void linf_partial_kernel(long long n, const double2* __restrict__ x, double* part) {
+  pdl_prologue();
   double m = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double2 a = x[i];
@@ -128,6 +133,7 @@ __global__ __launch_bounds__(256) void linf_partial_kernel(long long n, const do
 
 __global__ __launch_bounds__(256) void nonfinite_partial_kernel(long long n, const double2* __restrict__ x,
                                                                 double* part) {
+  pdl_prologue();
   double m = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double2 a = x[i];
@@ -139,6 +145,7 @@ __global__ __launch_bounds__(256) void nonfinite_partial_kernel(long long n, con
 
 __global__ __launch_bounds__(1024) void reduce_final_kernel(const double* __restrict__ part, int n, int op,
                                                             double* slot) {
+  pdl_prologue();
   double v = op == 0 ? 0.0 : -INFINITY;
   for (int i = threadIdx.x; i < n; i += blockDim.x) v = op == 0 ? v + part[i] : fmax(v, part[i]);
   v = op == 0 ? block_sum(v) : block_max(v);
@@ -153,13 +160,13 @@ static int red_grid(long long n) {
 
 int launch_inner_partial(long long n, const double2* x, const double2* y, double* part, cudaStream_t s) {
   const int g = red_grid(n);
-  inner_partial_kernel<<<g, 256, 0, s>>>(n, x, y, part);
+  pdl_launch(inner_partial_kernel, g, 256, 0, s, n, x, y, part);
   LDDMM_LAUNCH_CHECK();
   return g;
 }
 int launch_linf_partial(long long n, const double2* x, double* part, cudaStream_t s) {
   const int g = red_grid(n);
-  linf_partial_kernel<<<g, 256, 0, s>>>(n, x, part);
+  pdl_launch(linf_partial_kernel, g, 256, 0, s, n, x, part);
   LDDMM_LAUNCH_CHECK();
   return g;
 }
@@ -168,6 +175,7 @@ int launch_linf_partial(long long n, const double2* x, double* part, cudaStream_
 // the same max of 0/1 flags as nonfinite_partial + reduce_final.
 __global__ __launch_bounds__(256) void nonfinite_flag_kernel(long long n, const double2* __restrict__ x, double* part,
                                                              double* slot) {
+  pdl_prologue();
   unsigned* counter = reinterpret_cast<unsigned*>(part + kReduceBlocks);
   __shared__ bool last;
   double m = 0.0;
@@ -195,18 +203,18 @@ __global__ __launch_bounds__(256) void nonfinite_flag_kernel(long long n, const 
 }
 
 void launch_nonfinite_flag(long long n, const double2* x, double* part, double* slot, cudaStream_t s) {
-  nonfinite_flag_kernel<<<red_grid(n), 256, 0, s>>>(n, x, part, slot);
+  pdl_launch(nonfinite_flag_kernel, red_grid(n), 256, 0, s, n, x, part, slot);
   LDDMM_LAUNCH_CHECK();
 }
 
 int launch_nonfinite_partial(long long n, const double2* x, double* part, cudaStream_t s) {
   const int g = red_grid(n);
-  nonfinite_partial_kernel<<<g, 256, 0, s>>>(n, x, part);
+  pdl_launch(nonfinite_partial_kernel, g, 256, 0, s, n, x, part);
   LDDMM_LAUNCH_CHECK();
   return g;
 }
 void launch_reduce_final(const double* part, int nparts, int op, double* slot, cudaStream_t s) {
-  reduce_final_kernel<<<1, 1024, 0, s>>>(part, nparts, op, slot);
+  pdl_launch(reduce_final_kernel, 1, 1024, 0, s, part, nparts, op, slot);
   LDDMM_LAUNCH_CHECK();
 }
 

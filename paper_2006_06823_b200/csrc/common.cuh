@@ -6,6 +6,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -55,6 +57,42 @@ struct NvtxRange {
 #define LDDMM_NVTX_CAT2(a, b) a##b
 #define LDDMM_NVTX_CAT(a, b) LDDMM_NVTX_CAT2(a, b)
 #define LDDMM_NVTX(name) ::lddmm_b200::NvtxRange LDDMM_NVTX_CAT(nvtx_range_, __LINE__)(name)
+
+// Programmatic dependent launch (PDL).  Every engine kernel starts with pdl_prologue():
+// griddepcontrol.wait (no access to global memory before the preceding kernel in the
+// stream has completed and its writes are visible), then launch_dependents (the next
+// kernel may be scheduled now).  Kernels are launched through pdl_launch(), which sets
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's launch and CTA
+// ramp-up overlap its predecessor's tail instead of following it.  Without the
+// attribute (LDDMM_PDL=0) the two instructions are no-ops and launches are ordinary.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("LDDMM_PDL");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);  // errors surface in LDDMM_LAUNCH_CHECK
+}
 
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
 

@@ -315,6 +315,7 @@ __global__ __launch_bounds__(GP_NTH, 1) void gather_pipe_kernel(const __grid_con
                                                                 const float* __restrict__ disp,
                                                                 float* __restrict__ out, int Nx, int Ny, int Nz,
                                                                 float3 sc, int TY, int seg) {
+  pdl_prologue();
   extern __shared__ __align__(1024) float sm[];
   __shared__ __align__(8) unsigned long long full[GP_RING];
   __shared__ int relcnt[GP_RING];
@@ -494,7 +495,7 @@ void gp_launch(const float* coef, int ncomp, const float* disp, float* out, cons
                                     (int)GP_SMEM_MAX));
     attr_set[dev & 63] = true;
   }
-  gather_pipe_kernel<FG, P><<<dim3(nseg, tiles_y, 1), GP_NTH, smem, s>>>(tb, tr, coef, ncomp, disp, out, N[0], N[1],
+  pdl_launch(gather_pipe_kernel<FG, P>, dim3(nseg, tiles_y, 1), GP_NTH, smem, s, tb, tr, coef, ncomp, disp, out, N[0], N[1],
                                                                        N[2], sc, TY, seg);
   LDDMM_LAUNCH_CHECK();
 }

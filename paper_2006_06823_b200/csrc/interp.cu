@@ -66,6 +66,7 @@ __global__ __launch_bounds__(256) void gather_cubic_kernel(const float* __restri
                                                            const float* __restrict__ disp,
                                                            float* __restrict__ out, int Nx, int Ny, int Nz,
                                                            float3 sc) {
+  pdl_prologue();
   const long long N = (long long)Nx * Ny * Nz;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N;
        p += (long long)gridDim.x * blockDim.x) {
@@ -121,6 +122,7 @@ __global__ __launch_bounds__(GT_THREADS, 2) void gather_tiled_kernel(const float
                                                                   const float* __restrict__ disp,
                                                                   float* __restrict__ out, int Nx, int Ny, int Nz,
                                                                   float3 sc) {
+  pdl_prologue();
   extern __shared__ float sm[];
   const long long N = (long long)Nx * Ny * Nz;
   const int x0 = blockIdx.x * GT_X, y0 = blockIdx.y * GT_Y, z0 = blockIdx.z * GT_Z;
@@ -440,6 +442,7 @@ template <int FG, int TX, int TY, int NTH, int P, bool SHIFT>
 __global__ __launch_bounds__(NTH, 1) void gather_win_kernel(const float* __restrict__ coef, int F,
                                                             const float* __restrict__ disp, float* __restrict__ out,
                                                             int Nx, int Ny, int Nz, float3 sc) {
+  pdl_prologue();
   extern __shared__ __align__(16) float smw[];
   const long long N = (long long)Nx * Ny * Nz;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
@@ -533,6 +536,7 @@ template <int FG, int NTH, int P, bool SHIFT>
 __global__ __launch_bounds__(NTH, 1) void gather_march_kernel(const float* __restrict__ coef, int F,
                                                               const float* __restrict__ disp, float* __restrict__ out,
                                                               int Nx, int Ny, int Nz, float3 sc, int TY, int seg) {
+  pdl_prologue();
   constexpr int TYM = gm_tymax<FG, P>();
   constexpr int CVOL = (TYM + 2 * GW_H) * P;
   constexpr int SLOT = FG * CVOL;
@@ -609,7 +613,7 @@ static bool launch_gm_pitch(const float* coef, int ncomp, const float* disp, flo
       LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GW_SMEM_MAX));
       attr_set[dev & 63][k] = true;
     }
-    kern<<<grid, GM_NTH, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], sc, TY, seg);
+    pdl_launch(kern, grid, GM_NTH, smem, s, coef, ncomp, disp, out, N[0], N[1], N[2], sc, TY, seg);
   };
   if (FG == 3)
     go(gather_march_kernel<3, GM_NTH, P, SHIFT>, 2);
@@ -652,7 +656,7 @@ static bool launch_gw_pitch(const float* coef, int ncomp, const float* disp, flo
       LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GW_SMEM_MAX));
       attr_set[dev & 63][k] = true;
     }
-    kern<<<grid, GW_NTH, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], sc);
+    pdl_launch(kern, grid, GW_NTH, smem, s, coef, ncomp, disp, out, N[0], N[1], N[2], sc);
   };
   if (FG == 3)
     go(gather_win_kernel<3, GW_TX, GW_TY, GW_NTH, P, SHIFT>, 2);
@@ -719,11 +723,11 @@ void launch_gather_cubic_tiled(const float* coef, int ncomp, const float* disp, 
       attr_set[dev & 63] = true;
     }
     if (FG == 3)
-      gather_tiled_kernel<3><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
+      pdl_launch(gather_tiled_kernel<3>, grid, GT_THREADS, smem, s, coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
     else if (FG == 2)
-      gather_tiled_kernel<2><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
+      pdl_launch(gather_tiled_kernel<2>, grid, GT_THREADS, smem, s, coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
     else
-      gather_tiled_kernel<1><<<grid, GT_THREADS, smem, s>>>(coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
+      pdl_launch(gather_tiled_kernel<1>, grid, GT_THREADS, smem, s, coef, ncomp, disp, out, N[0], N[1], N[2], make_float3(1.f, 1.f, 1.f));
     LDDMM_LAUNCH_CHECK();
     return;
   }
@@ -739,16 +743,16 @@ static void launch_gather_global_scaled(const float* coef, int ncomp, const floa
     const float* c = coef + (long long)done * n;
     float* o = out + (long long)done * n;
     if (left >= 6) {
-      gather_cubic_kernel<6><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
+      pdl_launch(gather_cubic_kernel<6>, grid, 256, 0, s, c, disp, o, N[0], N[1], N[2], sc);
       done += 6;
     } else if (left >= 4) {
-      gather_cubic_kernel<4><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
+      pdl_launch(gather_cubic_kernel<4>, grid, 256, 0, s, c, disp, o, N[0], N[1], N[2], sc);
       done += 4;
     } else if (left >= 3) {
-      gather_cubic_kernel<3><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
+      pdl_launch(gather_cubic_kernel<3>, grid, 256, 0, s, c, disp, o, N[0], N[1], N[2], sc);
       done += 3;
     } else {
-      gather_cubic_kernel<1><<<grid, 256, 0, s>>>(c, disp, o, N[0], N[1], N[2], sc);
+      pdl_launch(gather_cubic_kernel<1>, grid, 256, 0, s, c, disp, o, N[0], N[1], N[2], sc);
       done += 1;
     }
     LDDMM_LAUNCH_CHECK();
@@ -767,6 +771,7 @@ void launch_gather_cubic_global(const float* coef, int ncomp, const float* disp,
 __global__ __launch_bounds__(256) void departure_kernel(const float* __restrict__ vg, const float* __restrict__ vc,
                                                         float dtx, float dty, float dtz, float* __restrict__ df,
                                                         float* __restrict__ db, int Nx, int Ny, int Nz) {
+  pdl_prologue();
   const long long N = (long long)Nx * Ny * Nz;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N;
        p += (long long)gridDim.x * blockDim.x) {
@@ -794,6 +799,7 @@ __global__ __launch_bounds__(256) void departure_kernel(const float* __restrict_
 // D = sg * dt/2 * (v_traced(X*) + v_grid) in grid units, vm = v_traced(X*) gathered
 __global__ void departure_combine_kernel(long long n, const float* __restrict__ vg, const float* __restrict__ vm,
                                          float dtx, float dty, float dtz, float sg, float* __restrict__ o) {
+  pdl_prologue();
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
     const float ux = vg[p] * dtx, uy = vg[n + p] * dty, uz = vg[2 * n + p] * dtz;
     o[p] = sg * 0.5f * (vm[p] * dtx + ux);
@@ -810,7 +816,7 @@ void launch_departure_dir(const float* vgrid, const float* vcoef, double dt, con
   const long long n = (long long)N[0] * N[1] * N[2];
   const float dtx = (float)(dt / h[0]), dty = (float)(dt / h[1]), dtz = (float)(dt / h[2]);
   launch_gather_scaled(vcoef, 3, vgrid, sg * dtx, sg * dty, sg * dtz, vm, N, s);
-  departure_combine_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, vgrid, vm, dtx, dty, dtz, sg, out);
+  pdl_launch(departure_combine_kernel, grid_for(n, 256), 256, 0, s, n, vgrid, vm, dtx, dty, dtz, sg, out);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -844,6 +850,7 @@ void launch_warp_by_displacement(const float* coef, int ncomp, const float* disp
 __global__ void warp_nearest_kernel(const float* __restrict__ f, int ncomp, const float* __restrict__ disp,
                                     double hx, double hy, double hz, float* __restrict__ out, int Nx, int Ny,
                                     int Nz) {
+  pdl_prologue();
   const long long N = (long long)Nx * Ny * Nz;
   GRID_STRIDE(p, N) {
     const int k = (int)(p % Nz);
@@ -864,7 +871,7 @@ __global__ void warp_nearest_kernel(const float* __restrict__ f, int ncomp, cons
 void launch_warp_nearest(const float* f, int ncomp, const float* disp_phys, const double* h, float* out,
                          const int* N, cudaStream_t s) {
   const long long n = (long long)N[0] * N[1] * N[2];
-  warp_nearest_kernel<<<grid_for(n, 256), 256, 0, s>>>(f, ncomp, disp_phys, h[0], h[1], h[2], out, N[0], N[1],
+  pdl_launch(warp_nearest_kernel, grid_for(n, 256), 256, 0, s, f, ncomp, disp_phys, h[0], h[1], h[2], out, N[0], N[1],
                                                        N[2]);
   LDDMM_LAUNCH_CHECK();
 }
@@ -877,6 +884,7 @@ void launch_warp_nearest(const float* f, int ncomp, const float* disp_phys, cons
 template <typename T>
 __global__ void prefilter_axis_kernel(T* __restrict__ v, int n, long long stride, long long lines,
                                       long long outer_stride) {
+  pdl_prologue();
   for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < lines;
        l += (long long)gridDim.x * blockDim.x) {
     const long long o = l / stride, s = l % stride;
@@ -920,7 +928,7 @@ static void prefilter3d(T* f, const int* N, cudaStream_t s) {
     long long stride = 1;
     for (int b = a + 1; b < 3; ++b) stride *= N[b];
     const long long lines = total / n;
-    prefilter_axis_kernel<T><<<grid_for(lines, 128, 32), 128, 0, s>>>(f, n, stride, lines, stride * n);
+    pdl_launch(prefilter_axis_kernel<T>, grid_for(lines, 128, 32), 128, 0, s, f, n, stride, lines, stride * n);
     LDDMM_LAUNCH_CHECK();
   }
 }
@@ -932,6 +940,7 @@ static void prefilter3d(T* f, const int* N, cudaStream_t s) {
 // with D the inverse DFT of i*omega (grid Nyquist zeroed), built in fp64 on the host.
 __global__ void circulant_axis_kernel(const double* __restrict__ in, double* __restrict__ out,
                                       const double* __restrict__ D, int n, long long stride, long long total) {
+  pdl_prologue();
   extern __shared__ double sD[];
   for (int t = threadIdx.x; t < n; t += blockDim.x) sD[t] = D[t];
   __syncthreads();
@@ -960,6 +969,7 @@ constexpr int CR = 8;
 __global__ void circulant_axis_blocked_kernel(const double* __restrict__ in, double* __restrict__ out,
                                               const double* __restrict__ D, int n, long long stride,
                                               long long work) {
+  pdl_prologue();
   extern __shared__ double sD[];
   for (int t = threadIdx.x; t < n; t += blockDim.x) sD[t] = D[t];
   __syncthreads();
@@ -1019,12 +1029,12 @@ void launch_circulant_axis_f64(const double* in, double* out, const double* D, i
   const long long total = (long long)N[0] * N[1] * N[2];
   if (N[axis] >= 8) {
     const long long work = total / N[axis] * ((N[axis] + CR - 1) / CR);
-    circulant_axis_blocked_kernel<<<grid_for(work, 256, 8), 256, N[axis] * sizeof(double), s>>>(in, out, D, N[axis],
+    pdl_launch(circulant_axis_blocked_kernel, grid_for(work, 256, 8), 256, N[axis] * sizeof(double), s, in, out, D, N[axis],
                                                                                                stride, work);
     LDDMM_LAUNCH_CHECK();
     return;
   }
-  circulant_axis_kernel<<<grid_for(total, 256, 16), 256, N[axis] * sizeof(double), s>>>(in, out, D, N[axis],
+  pdl_launch(circulant_axis_kernel, grid_for(total, 256, 16), 256, N[axis] * sizeof(double), s, in, out, D, N[axis],
                                                                                         stride, total);
   LDDMM_LAUNCH_CHECK();
 }

@@ -11,17 +11,19 @@
 namespace lddmm_b200 {
 
 __global__ void f64_to_f32_kernel(long long n, const double* __restrict__ in, float* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) out[i] = (float)in[i];
 }
 __global__ void f32_to_f64_kernel(long long n, const float* __restrict__ in, double* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) out[i] = (double)in[i];
 }
 void launch_f64_to_f32(long long n, const double* in, float* out, cudaStream_t s) {
-  f64_to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, in, out);
+  pdl_launch(f64_to_f32_kernel, grid_for(n, 256), 256, 0, s, n, in, out);
   LDDMM_LAUNCH_CHECK();
 }
 void launch_f32_to_f64(long long n, const float* in, double* out, cudaStream_t s) {
-  f32_to_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, in, out);
+  pdl_launch(f32_to_f64_kernel, grid_for(n, 256), 256, 0, s, n, in, out);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -34,6 +36,7 @@ static int red_grid(long long n) {
 __global__ __launch_bounds__(256) void residual_kernel(long long n, const float* __restrict__ m1,
                                                        const float* __restrict__ I1, float* __restrict__ res,
                                                        double* part) {
+  pdl_prologue();
   double s = 0.0;
   GRID_STRIDE(i, n) {
     const float r = m1[i] - I1[i];
@@ -45,12 +48,13 @@ __global__ __launch_bounds__(256) void residual_kernel(long long n, const float*
 }
 int launch_residual(long long n, const float* m1, const float* I1, float* res, double* part, cudaStream_t s) {
   const int g = red_grid(n);
-  residual_kernel<<<g, 256, 0, s>>>(n, m1, I1, res, part);
+  pdl_launch(residual_kernel, g, 256, 0, s, n, m1, I1, res, part);
   LDDMM_LAUNCH_CHECK();
   return g;
 }
 
 __global__ __launch_bounds__(256) void sumsq_kernel(long long n, const float* __restrict__ x, double* part) {
+  pdl_prologue();
   double s = 0.0;
   GRID_STRIDE(i, n) s += (double)x[i] * (double)x[i];
   s = block_sum(s);
@@ -58,12 +62,13 @@ __global__ __launch_bounds__(256) void sumsq_kernel(long long n, const float* __
 }
 int launch_sumsq_partial(long long n, const float* x, double* part, cudaStream_t s) {
   const int g = red_grid(n);
-  sumsq_kernel<<<g, 256, 0, s>>>(n, x, part);
+  pdl_launch(sumsq_kernel, g, 256, 0, s, n, x, part);
   LDDMM_LAUNCH_CHECK();
   return g;
 }
 
 __global__ __launch_bounds__(256) void absmax_kernel(long long n, const float* __restrict__ x, double* part) {
+  pdl_prologue();
   double m = 0.0;
   GRID_STRIDE(i, n) m = fmax(m, (double)fabsf(x[i]));
   m = block_max(m);
@@ -71,13 +76,14 @@ __global__ __launch_bounds__(256) void absmax_kernel(long long n, const float* _
 }
 int launch_absmax_partial(long long n, const float* x, double* part, cudaStream_t s) {
   const int g = red_grid(n);
-  absmax_kernel<<<g, 256, 0, s>>>(n, x, part);
+  pdl_launch(absmax_kernel, g, 256, 0, s, n, x, part);
   LDDMM_LAUNCH_CHECK();
   return g;
 }
 
 __global__ void scale_vec_kernel(long long n, const float* __restrict__ res, float c, const float* __restrict__ g,
                                  float* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) {
     const float r = res[i] * c;
     out[i] = r * g[i];
@@ -86,12 +92,13 @@ __global__ void scale_vec_kernel(long long n, const float* __restrict__ res, flo
   }
 }
 void launch_scale_vec(long long n, const float* res, double c, const float* g, float* out, cudaStream_t s) {
-  scale_vec_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, res, (float)c, g, out);
+  pdl_launch(scale_vec_kernel, grid_for(n, 256), 256, 0, s, n, res, (float)c, g, out);
   LDDMM_LAUNCH_CHECK();
 }
 
 __global__ void dr1_kernel(long long n, const float* __restrict__ g, const float* __restrict__ du, float c,
                            float* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) {
     const float g0 = g[i], g1 = g[n + i], g2 = g[2 * n + i];
     float dm = 0.f;
@@ -105,13 +112,14 @@ __global__ void dr1_kernel(long long n, const float* __restrict__ g, const float
   }
 }
 void launch_dr1(long long n, const float* g, const float* du, double c, float* out, cudaStream_t s) {
-  dr1_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, g, du, (float)c, out);
+  pdl_launch(dr1_kernel, grid_for(n, 256), 256, 0, s, n, g, du, (float)c, out);
   LDDMM_LAUNCH_CHECK();
 }
 
 // dlam1 = ((-1 * sum_b g_b du_b) * c)   (variants.hpp:326-327, state branch)
 __global__ void dlam1_kernel(long long n, const float* __restrict__ g, const float* __restrict__ du, float c,
                              float* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) {
     float dm = 0.f;
     dm += g[i] * du[i];
@@ -121,7 +129,7 @@ __global__ void dlam1_kernel(long long n, const float* __restrict__ g, const flo
   }
 }
 void launch_dlam1(long long n, const float* g, const float* du, double c, float* out, cudaStream_t s) {
-  dlam1_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, g, du, (float)c, out);
+  pdl_launch(dlam1_kernel, grid_for(n, 256), 256, 0, s, n, g, du, (float)c, out);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -133,6 +141,7 @@ void launch_dlam1(long long n, const float* g, const float* du, double c, float*
 //  op 4 s*s : a = s[n], b = t[n]                    -> acc    += s t
 __global__ void products_kernel(int op, long long n, const float* __restrict__ A, const float* __restrict__ B,
                                 float* __restrict__ acc, float w, int init) {
+  pdl_prologue();
   GRID_STRIDE(i, n) {
     if (op == 0 || op == 1) {
       float o[3] = {0.f, 0.f, 0.f};
@@ -165,13 +174,14 @@ __global__ void products_kernel(int op, long long n, const float* __restrict__ A
 }
 void launch_products(int op, long long n, const float* a, const float* b, float* acc, float w, bool init,
                      cudaStream_t s) {
-  products_kernel<<<grid_for(n, 256), 256, 0, s>>>(op, n, a, b, acc, w, init ? 1 : 0);
+  pdl_launch(products_kernel, grid_for(n, 256), 256, 0, s, op, n, a, b, acc, w, init ? 1 : 0);
   LDDMM_LAUNCH_CHECK();
 }
 
 __global__ void jac_batch_kernel(int transpose, int nn, long long M, const float* __restrict__ D,
                                  const float* __restrict__ W, long long wstride, float* __restrict__ out,
                                  long long ostride, NodeWeights wts, int init) {
+  pdl_prologue();
   GRID_STRIDE(i, M) {
     float acc[3] = {0.f, 0.f, 0.f};
     if (ostride == 0 && !init) {
@@ -210,7 +220,7 @@ __global__ void jac_batch_kernel(int transpose, int nn, long long M, const float
 void launch_jac_batch(bool transpose, int nn, long long M, const float* derivs, const float* w,
                       long long w_node_stride, float* out, long long out_stride, NodeWeights wts, bool init,
                       cudaStream_t s) {
-  jac_batch_kernel<<<grid_for(M, 256), 256, 0, s>>>(transpose ? 1 : 0, nn, M, derivs, w, w_node_stride, out,
+  pdl_launch(jac_batch_kernel, grid_for(M, 256), 256, 0, s, transpose ? 1 : 0, nn, M, derivs, w, w_node_stride, out,
                                                     out_stride, wts, init ? 1 : 0);
   LDDMM_LAUNCH_CHECK();
 }
@@ -227,6 +237,7 @@ __device__ __forceinline__ double det3(const float* du, long long n, long long i
 
 __global__ __launch_bounds__(256) void jacdet_minmax_kernel(long long n, const float* __restrict__ du,
                                                             double* pmin, double* pmax) {
+  pdl_prologue();
   double lo = 1e300, hi = -1e300;
   GRID_STRIDE(i, n) {
     const double d = det3(du, n, i);
@@ -242,15 +253,16 @@ __global__ __launch_bounds__(256) void jacdet_minmax_kernel(long long n, const f
 }
 int launch_jacdet_minmax(long long n, const float* du, double* part_min, double* part_max, cudaStream_t s) {
   const int g = red_grid(n);
-  jacdet_minmax_kernel<<<g, 256, 0, s>>>(n, du, part_min, part_max);
+  pdl_launch(jacdet_minmax_kernel, g, 256, 0, s, n, du, part_min, part_max);
   LDDMM_LAUNCH_CHECK();
   return g;
 }
 __global__ void jacdet_kernel(long long n, const float* __restrict__ du, float* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) out[i] = (float)det3(du, n, i);
 }
 void launch_jacdet(long long n, const float* du, float* out, cudaStream_t s) {
-  jacdet_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, du, out);
+  pdl_launch(jacdet_kernel, grid_for(n, 256), 256, 0, s, n, du, out);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -262,6 +274,7 @@ __global__ __launch_bounds__(256) void dice_counts_kernel(long long n, const flo
                                                           const float* __restrict__ b,
                                                           const float* __restrict__ labels, int nl,
                                                           unsigned long long* counts) {
+  pdl_prologue();
   __shared__ unsigned int sc[3 * DICE_MAXL];
   __shared__ float sl[DICE_MAXL];
   for (int t = threadIdx.x; t < 3 * DICE_MAXL; t += blockDim.x) sc[t] = 0u;
@@ -286,24 +299,26 @@ void launch_dice_counts(long long n, const float* a, const float* b, const float
   LDDMM_CUDA(cudaMemsetAsync(counts, 0, 3 * (size_t)nl * sizeof(unsigned long long), s));
   for (int l0 = 0; l0 < nl; l0 += DICE_MAXL) {
     const int m = nl - l0 < DICE_MAXL ? nl - l0 : DICE_MAXL;
-    dice_counts_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, a, b, labels + l0, m, counts + 3 * l0);
+    pdl_launch(dice_counts_kernel, grid_for(n, 256), 256, 0, s, n, a, b, labels + l0, m, counts + 3 * l0);
     LDDMM_LAUNCH_CHECK();
   }
 }
 
 __global__ void affine_kernel(long long n, const float* __restrict__ x, float a, float b, float* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) out[i] = a * x[i] + b;
 }
 void launch_affine_f32(long long n, const float* x, float a, float b, float* out, cudaStream_t s) {
-  affine_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, x, a, b, out);
+  pdl_launch(affine_kernel, grid_for(n, 256), 256, 0, s, n, x, a, b, out);
   LDDMM_LAUNCH_CHECK();
 }
 __global__ void mul_kernel(long long n, const float* __restrict__ x, const float* __restrict__ y,
                            float* __restrict__ out) {
+  pdl_prologue();
   GRID_STRIDE(i, n) out[i] = x[i] * y[i];
 }
 void launch_mul_f32(long long n, const float* x, const float* y, float* out, cudaStream_t s) {
-  mul_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, x, y, out);
+  pdl_launch(mul_kernel, grid_for(n, 256), 256, 0, s, n, x, y, out);
   LDDMM_LAUNCH_CHECK();
 }
 

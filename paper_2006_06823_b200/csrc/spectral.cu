@@ -71,6 +71,7 @@ __device__ __forceinline__ float2 prep_value(const PrepArgs& a, int f, int fx, i
 
 __global__ void band_prep_kernel(PrepArgs a, int Kx, int Ky, int Kz, int Nx, int Ny, int Nz, double wx,
                                  double wy, double wz, float2* __restrict__ D) {
+  pdl_prologue();
   const int H = Kz / 2;
   const long long per = (long long)Kx * Ky * H;
   const long long total = per * a.nf;
@@ -90,6 +91,7 @@ __global__ void band_prep_kernel(PrepArgs a, int Kx, int Ky, int Kz, int Nx, int
 // finalize: G3 half band (fp32) -> full band fp64 with Hermitian completion
 
 __global__ void band_finalize_kernel(FinArgs a, int Kx, int Ky, int Kz, const float2* __restrict__ G) {
+  pdl_prologue();
   const int H = Kz / 2;
   const long long per = (long long)Kx * Ky * Kz;
   const long long total = per * a.nf;
@@ -145,6 +147,7 @@ __global__ __launch_bounds__(256) void cgemm_kernel(const float2* __restrict__ A
                                                     const float2* __restrict__ B, long long sB, int ldb,
                                                     float2* __restrict__ C, long long sC, int ldc, int M,
                                                     int N, int K) {
+  pdl_prologue();
   __shared__ float2 As[2][CG_BK][CG_BM + 1];
   __shared__ float2 Bs[2][CG_BK][CG_BN + 1];
   const int tid = threadIdx.x;
@@ -219,6 +222,7 @@ __global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__
                                                        const float* __restrict__ B, int ldb,
                                                        float* __restrict__ C, int ldc, long long sC, int M,
                                                        int N, int K) {
+  pdl_prologue();
   constexpr int BM = 128, BK = 16, NT = BN * 4, TXN = BN / 4;
   __shared__ __align__(16) float As[BK][BM + 4];
   __shared__ __align__(16) float Bs[BK][BN];
@@ -281,14 +285,14 @@ __global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__
 
 void launch_band_prep(const PrepArgs& a, const DftPlan& p, float2* D, cudaStream_t s) {
   const long long total = (long long)p.K[0] * p.K[1] * (p.K[2] / 2) * a.nf;
-  band_prep_kernel<<<grid_for(total, 256), 256, 0, s>>>(a, p.K[0], p.K[1], p.K[2], p.N[0], p.N[1], p.N[2],
+  pdl_launch(band_prep_kernel, grid_for(total, 256), 256, 0, s, a, p.K[0], p.K[1], p.K[2], p.N[0], p.N[1], p.N[2],
                                                         p.omega_unit[0], p.omega_unit[1], p.omega_unit[2], D);
   LDDMM_LAUNCH_CHECK();
 }
 
 void launch_band_finalize(const FinArgs& a, const DftPlan& p, const float2* G, cudaStream_t s) {
   const long long total = (long long)p.K[0] * p.K[1] * p.K[2] * a.nf;
-  band_finalize_kernel<<<grid_for(total, 256), 256, 0, s>>>(a, p.K[0], p.K[1], p.K[2], G);
+  pdl_launch(band_finalize_kernel, grid_for(total, 256), 256, 0, s, a, p.K[0], p.K[1], p.K[2], G);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -344,6 +348,7 @@ __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restric
                                                          float2* __restrict__ C, long long sC, int ldc, int M, int N,
                                                          int K, int batch, const __grid_constant__ PrepCtx pc,
                                                          const __grid_constant__ FinCtx fc) {
+  pdl_prologue();
   constexpr bool PREP = MODE == 1, FIN = MODE == 2;
   extern __shared__ float2 sm2[];
   const int KP = K + 1;  // padded A row (bank spread across rows)
@@ -434,7 +439,7 @@ static void launch_cgemm_smem(const float2* A, int lda, const float2* B, long lo
         cudaFuncSetAttribute(cgemm_smem_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set[dev & 63] = true;
   }
-  cgemm_smem_kernel<MODE><<<batch, 256, smem, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, pc, fc);
+  pdl_launch(cgemm_smem_kernel<MODE>, batch, 256, smem, s, A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, pc, fc);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -447,7 +452,7 @@ void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int l
     return;
   }
   dim3 grid(ceil_div(N, CG_BN), ceil_div(M, CG_BM), batch);
-  cgemm_kernel<<<grid, 256, 0, s>>>(A, lda, B, sB, ldb, C, sC, ldc, M, N, K);
+  pdl_launch(cgemm_kernel, grid, 256, 0, s, A, lda, B, sB, ldb, C, sC, ldc, M, N, K);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -455,10 +460,10 @@ void launch_sgemm(const float* A, int lda, long long sA, const float* B, int ldb
                   long long sC, int M, int N, int K, int batch, cudaStream_t s) {
   if (N <= 32) {
     dim3 grid(ceil_div(N, 32), ceil_div(M, 128), batch);
-    sgemm_kernel<32><<<grid, 128, 0, s>>>(A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
+    pdl_launch(sgemm_kernel<32>, grid, 128, 0, s, A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
   } else {
     dim3 grid(ceil_div(N, 64), ceil_div(M, 128), batch);
-    sgemm_kernel<64><<<grid, 256, 0, s>>>(A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
+    pdl_launch(sgemm_kernel<64>, grid, 256, 0, s, A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
   }
   LDDMM_LAUNCH_CHECK();
 }

@@ -53,6 +53,7 @@ __global__ __launch_bounds__(256) void tc3_gemm_kernel(const float* __restrict__
                                                        const float* __restrict__ Bsmall, int ldb,
                                                        float* __restrict__ C, int ldc, long long sC, int M, int N,
                                                        int K) {
+  pdl_prologue();
   constexpr int BM = 128;
   constexpr int WN = BN == 64 ? 2 : 1;  // warps along n
   constexpr int WMW = 8 / WN;           // warps along m
@@ -179,6 +180,7 @@ __global__ __launch_bounds__(256) void tc3_gemm_kernel(const float* __restrict__
 
 __global__ void tf32_split_kernel(const float* __restrict__ in, float* __restrict__ big, float* __restrict__ small,
                                   long long n) {
+  pdl_prologue();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const float x = in[i];
     const uint32_t b = f2tf32(x);
@@ -188,7 +190,7 @@ __global__ void tf32_split_kernel(const float* __restrict__ in, float* __restric
 }
 
 void launch_tf32_split(const float* in, float* big, float* small, long long n, cudaStream_t s) {
-  tf32_split_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, big, small, n);
+  pdl_launch(tf32_split_kernel, grid_for(n, 256), 256, 0, s, in, big, small, n);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -196,10 +198,10 @@ void launch_tc3_gemm(const float* A, int lda, long long sA, const float* Bbig, c
                      int ldc, long long sC, int M, int N, int K, int batch, cudaStream_t s) {
   if (N <= 32) {
     dim3 grid(ceil_div(N, 32), ceil_div(M, 128), batch);
-    tc3_gemm_kernel<32><<<grid, 256, 0, s>>>(A, lda, sA, Bbig, Bsmall, ldb, C, ldc, sC, M, N, K);
+    pdl_launch(tc3_gemm_kernel<32>, grid, 256, 0, s, A, lda, sA, Bbig, Bsmall, ldb, C, ldc, sC, M, N, K);
   } else {
     dim3 grid(ceil_div(N, 64), ceil_div(M, 128), batch);
-    tc3_gemm_kernel<64><<<grid, 256, 0, s>>>(A, lda, sA, Bbig, Bsmall, ldb, C, ldc, sC, M, N, K);
+    pdl_launch(tc3_gemm_kernel<64>, grid, 256, 0, s, A, lda, sA, Bbig, Bsmall, ldb, C, ldc, sC, M, N, K);
   }
   LDDMM_LAUNCH_CHECK();
 }

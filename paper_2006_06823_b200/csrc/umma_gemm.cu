@@ -105,6 +105,7 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
                                                                     float* __restrict__ C, long long sC, int M,
                                                                     int N, int NP, int K, int nb, int nsplit,
                                                                     const __grid_constant__ CUtensorMap tmC) {
+  pdl_prologue();
   const int KC = K / 4;
   const uint32_t LBO = 128, SBO = (uint32_t)KC * 128;
   const int half = (int)blockIdx.x % nsplit;
@@ -308,6 +309,7 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
                                                                       const float* __restrict__ Bbig_c,
                                                                       const float* __restrict__ Bsm_c,
                                                                       float* __restrict__ C, int M, int Kpad) {
+  pdl_prologue();
   constexpr int CH = 128 * ZP_KC;  // floats per chunk buffer
   constexpr uint32_t LBO_B = 128;
   constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
@@ -458,6 +460,7 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
 // Tz_p big/small [K][N] row-major -> canonical K-major [N][Kpad], rows k >= K zero
 __global__ void umma_zproj_prep_kernel(const float* __restrict__ Bbig, const float* __restrict__ Bsm, int K, int N,
                                        int Kpad, float* __restrict__ Cbig, float* __restrict__ Csm) {
+  pdl_prologue();
   const long long total = (long long)N * Kpad;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
     const int n = (int)(e / Kpad), k = (int)(e - (long long)n * Kpad);
@@ -501,7 +504,7 @@ bool umma_zproject_fits(int K, int N) {
 void launch_umma_zproj_prep(const float* Bbig, const float* Bsm, int K, int N, float* Cbig, float* Csm,
                             cudaStream_t s) {
   const int Kpad = umma_zproject_kpad(K);
-  umma_zproj_prep_kernel<<<grid_for((long long)N * Kpad, 256), 256, 0, s>>>(Bbig, Bsm, K, N, Kpad, Cbig, Csm);
+  pdl_launch(umma_zproj_prep_kernel, grid_for((long long)N * Kpad, 256), 256, 0, s, Bbig, Bsm, K, N, Kpad, Cbig, Csm);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -529,7 +532,7 @@ void launch_umma_zproject(const float* A, const float* Bbig_c, const float* Bsm_
       LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
       set[dev & 63][slot] = true;
     }
-    kern<<<grid, ZP_THREADS, smem, s>>>(tm, Bbig_c, Bsm_c, C, M, umma_zproject_kpad(K));
+    pdl_launch(kern, grid, ZP_THREADS, smem, s, tm, Bbig_c, Bsm_c, C, M, umma_zproject_kpad(K));
   };
   const bool deep = umma_zproject_deep(N, K);
   if (N == 32)
@@ -542,6 +545,7 @@ void launch_umma_zproject(const float* A, const float* Bbig_c, const float* Bsm_
 // B [K][N] (big / small TF32 parts, row-major) -> canonical K-major [NP][K], zero padded
 __global__ void umma_canon_b_kernel(const float* __restrict__ Bbig, const float* __restrict__ Bsm, int K, int N,
                                     int NP, float* __restrict__ Cbig, float* __restrict__ Csm) {
+  pdl_prologue();
   const long long total = (long long)NP * K;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
     const int n = (int)(e / K), k = (int)(e - (long long)n * K);
@@ -582,7 +586,7 @@ bool umma_zembed_fits(int N, int K) {
 void launch_umma_canon_b(const float* Bbig, const float* Bsm, int K, int N, float* Cbig, float* Csm,
                          cudaStream_t s) {
   const int NP = umma_padded_n(N);
-  umma_canon_b_kernel<<<grid_for((long long)NP * K, 256), 256, 0, s>>>(Bbig, Bsm, K, N, NP, Cbig, Csm);
+  pdl_launch(umma_canon_b_kernel, grid_for((long long)NP * K, 256), 256, 0, s, Bbig, Bsm, K, N, NP, Cbig, Csm);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -616,7 +620,7 @@ void launch_umma_zembed(const float* A, long long sA, const float* Bbig_c, const
       LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
       set[dev & 63][slot] = true;
     }
-    kern<<<grid, UZ_THREADS, smem, s>>>(A, sA, Bbig_c, Bsm_c, C, sC, M, N, NP, K, nb, nsplit, tmC);
+    pdl_launch(kern, grid, UZ_THREADS, smem, s, A, sA, Bbig_c, Bsm_c, C, sC, M, N, NP, K, nb, nsplit, tmC);
   };
   const int NPS = nsplit > 1 ? N / nsplit : NP;
   if (NPS <= 32)
