@@ -58,16 +58,20 @@ struct NvtxRange {
 #define LDDMM_NVTX_CAT(a, b) LDDMM_NVTX_CAT2(a, b)
 #define LDDMM_NVTX(name) ::lddmm_b200::NvtxRange LDDMM_NVTX_CAT(nvtx_range_, __LINE__)(name)
 
-// Programmatic dependent launch (PDL).  Every engine kernel starts with pdl_prologue():
+// Programmatic dependent launch (PDL).  Every engine kernel starts with pdl_prologue()
+// (kernels with constant set-up — twiddle tables, TMEM allocation, mbarriers — do that
+// first and call pdl_wait() / pdl_trigger() after it):
 // griddepcontrol.wait (no access to global memory before the preceding kernel in the
 // stream has completed and its writes are visible), then launch_dependents (the next
 // kernel may be scheduled now).  Kernels are launched through pdl_launch(), which sets
 // cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's launch and CTA
 // ramp-up overlap its predecessor's tail instead of following it.  Without the
 // attribute (LDDMM_PDL=0) the two instructions are no-ops and launches are ordinary.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_prologue() {
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  pdl_wait();
+  pdl_trigger();
 }
 
 inline bool pdl_enabled() {

@@ -348,17 +348,20 @@ __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restric
                                                          float2* __restrict__ C, long long sC, int ldc, int M, int N,
                                                          int K, int batch, const __grid_constant__ PrepCtx pc,
                                                          const __grid_constant__ FinCtx fc) {
-  pdl_prologue();
   constexpr bool PREP = MODE == 1, FIN = MODE == 2;
   extern __shared__ float2 sm2[];
   const int KP = K + 1;  // padded A row (bank spread across rows)
   float2* As = sm2;
   float2* Bs = sm2 + (long long)M * KP;
-  // cp.async (8-byte) copies: every element in flight at once, no register round trip
+  // cp.async (8-byte) copies: every element in flight at once, no register round trip.
+  // A is a twiddle table (constant): staged before the PDL wait, overlapping the
+  // preceding kernel's tail.
   for (int e = threadIdx.x; e < M * K; e += blockDim.x) {
     const int m = e / K, k = e - (e / K) * K;
     cp_async8_f2(As + m * KP + k, A + (long long)m * lda + k);
   }
+  pdl_wait();
+  pdl_trigger();
   const int tn = (N + 1) / 2, tiles = ((M + 1) / 2) * tn;
   for (int b = blockIdx.x; b < batch; b += gridDim.x) {
     __syncthreads();

@@ -105,7 +105,6 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
                                                                     float* __restrict__ C, long long sC, int M,
                                                                     int N, int NP, int K, int nb, int nsplit,
                                                                     const __grid_constant__ CUtensorMap tmC) {
-  pdl_prologue();
   const int KC = K / 4;
   const uint32_t LBO = 128, SBO = (uint32_t)KC * 128;
   const int half = (int)blockIdx.x % nsplit;
@@ -139,6 +138,9 @@ __global__ __launch_bounds__(UZ_THREADS, 1) void umma_zembed_kernel(const float*
       reinterpret_cast<float4*>(Bs)[e] = __ldg(bs + e);
     }
   }
+  // TMEM, barriers and the (constant) twiddle operand are set up before the PDL wait
+  pdl_wait();
+  pdl_trigger();
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -309,7 +311,6 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
                                                                       const float* __restrict__ Bbig_c,
                                                                       const float* __restrict__ Bsm_c,
                                                                       float* __restrict__ C, int M, int Kpad) {
-  pdl_prologue();
   constexpr int CH = 128 * ZP_KC;  // floats per chunk buffer
   constexpr uint32_t LBO_B = 128;
   constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
@@ -344,6 +345,9 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
     reinterpret_cast<float4*>(Bb)[e] = __ldg(reinterpret_cast<const float4*>(Bbig_c) + e);
     reinterpret_cast<float4*>(Bs)[e] = __ldg(reinterpret_cast<const float4*>(Bsm_c) + e);
   }
+  // TMEM, barriers and the (constant) twiddle operand are set up before the PDL wait
+  pdl_wait();
+  pdl_trigger();
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
