@@ -219,3 +219,22 @@ void launch_reduce_final(const double* part, int nparts, int op, double* slot, c
 }
 
 }  // namespace lddmm_b200
+
+namespace lddmm_b200 {
+
+// *mismatch = number of CTAs that saw a[i] != b[i] bitwise (0: the arrays are equal)
+__global__ void equal_flag_kernel(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                                  unsigned long long* mismatch) {
+  pdl_prologue();
+  bool same = true;
+  GRID_STRIDE(i, n) same = same && (__double_as_longlong(a[i]) == __double_as_longlong(b[i]));
+  if (__syncthreads_or(!same) && threadIdx.x == 0) atomicAdd(mismatch, 1ULL);
+}
+
+void launch_equal_flag(long long n, const double* a, const double* b, unsigned long long* mismatch, cudaStream_t s) {
+  LDDMM_CUDA(cudaMemsetAsync(mismatch, 0, sizeof(unsigned long long), s));
+  pdl_launch(equal_flag_kernel, grid_for(n, 256, 4), 256, 0, s, n, a, b, mismatch);
+  LDDMM_LAUNCH_CHECK();
+}
+
+}  // namespace lddmm_b200

@@ -123,6 +123,7 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   ugrid_.alloc(3 * N);
   trial_m1_.alloc(N);
   trial_res_.alloc(N);
+  if (trial_reuse_ok()) trial_u_.alloc((p.nt + 1) * V);
   I1_.alloc(N);
   I0f_.alloc(N);
   I0coef_.alloc(4 * N);  // I0 spline coefficients followed by grad I0 spline coefficients
@@ -323,6 +324,7 @@ void Engine::set_images_device_f32(const float* I0, const float* I1) {
 // I0 (fp64 on device) -> I0 spline coefficients, grad I0 spline coefficients,
 // mse denominator.  I0f_ / I1_ already hold the fp32 images.
 void Engine::set_images_impl(const double* I0d) {
+  trial_valid_ = false;
   const long long N = npts();
   const float* I0 = I0f_.p;
   const float* I1 = I1_.p;
@@ -507,6 +509,47 @@ void Engine::advect(const double2* q, int ncomp, const float* dep, double2* out)
 // ---------------------------------------------------------------------------
 // provider (transport.hpp:109-218, stationary): spatial node, spline coefficients,
 // band divergence, departure points, cfl
+
+bool Engine::same_velocity(const double2* a, const double2* b) {
+  // slot 1 reinterpreted as the mismatch counter
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(slots_.p + 1);
+  launch_equal_flag(2 * vel_elems(), reinterpret_cast<const double*>(a), reinterpret_cast<const double*>(b), cnt,
+                    stream_);
+  LDDMM_CUDA(cudaMemcpyAsync(host_slots_ + 1, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  unsigned long long m = 0;
+  std::memcpy(&m, host_slots_ + 1, sizeof(m));
+  return m == 0;
+}
+
+// trial provider + u series -> the forward cache (buffer swaps), then the backward
+// departure of the same velocity (stationary SL: transport.hpp:176-187)
+void Engine::adopt_trial_provider(bool with_bwd) {
+  auto swapbuf = [](auto& a, auto& b) {
+    std::swap(a.p, b.p);
+    std::swap(a.n, b.n);
+  };
+  swapbuf(prov_.v, trial_prov_.v);
+  swapbuf(prov_.div, trial_prov_.div);
+  swapbuf(prov_.dep_fwd, trial_prov_.dep_fwd);
+  swapbuf(u_, trial_u_);
+  prov_.cfl = trial_prov_.cfl;
+  pullback_large_ = prov_.cfl * prob_.nt > 1.0;
+  prov_.has_bwd = false;
+  if (with_bwd) {
+    const long long N = npts(), K = kprod();
+    PrepArgs pa{};
+    pa.nf = 6;
+    for (int c = 0; c < 3; ++c) {
+      pa.f[c] = PrepField{prov_.v.p + c * K, SYM_NONE, 1.0};
+      pa.f[3 + c] = PrepField{prov_.v.p + c * K, SYM_PREFILTER, 1.0};
+    }
+    embed_fields(full_, pa, gridA_.p, D_.p, E1_.p, E2_.p);
+    launch_departure_dir(gridA_.p, gridA_.p + 3 * N, 1.0 / prob_.nt, h_, 1.f, prov_.dep_bwd.p, gridB_.p, full_.N,
+                         stream_);
+    prov_.has_bwd = true;
+  }
+}
 
 void Engine::provider_build(const double2* v, ProviderState& ps, bool with_bwd) {
   const long long N = npts(), K = kprod(), V = vec_elems();
@@ -812,7 +855,17 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
   LDDMM_NVTX(with_adjoint ? "forward+adjoint" : "forward");
   const long long V = vec_elems(), N = npts();
   have_cache_ = false;
-  provider_build(v, prov_, with_adjoint);
+  // The forward at the velocity of the line search's accepted trial (optimizer.hpp:219,
+  // after trial_energy at the same tv_axpy result) adopts the trial's provider and u
+  // series instead of recomputing them: the same kernels on the same inputs, so the
+  // values are identical; only the backward departures are added.
+  const bool reuse = prob_.variant == 2 && trial_reuse_ok() && trial_valid_ && same_velocity(v, trial_prov_.v.p);
+  trial_valid_ = false;
+  if (reuse) {
+    adopt_trial_provider(with_adjoint);
+  } else {
+    provider_build(v, prov_, with_adjoint);
+  }
   Energies e;
   e.cfl = prov_.cfl;
   double ss = 0.0;
@@ -821,7 +874,7 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
   } else if (prob_.variant == 1) {
     ss = forward_state(with_adjoint);
   } else {
-    solve_displacement_fwd(prov_, u_.p, true, nullptr);
+    if (!reuse) solve_displacement_fwd(prov_, u_.p, true, nullptr);
     warp_m1(u_.p + prob_.nt * V, m1_.p, res_.p, with_adjoint, &ss);
   }
   if (with_adjoint && prob_.variant == 2) {
@@ -843,10 +896,19 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
 double Engine::energy(const double2* v) {
   LDDMM_NVTX("energy (trial)");
   if (prob_.variant == 0) return energy_original(v);
+  trial_valid_ = false;  // set again only when this trial completes
   provider_build(v, trial_prov_, false);
-  solve_displacement_fwd(trial_prov_, nullptr, false, bt(11));
   double ss = 0.0;
-  warp_m1(bt(11), trial_m1_.p, trial_res_.p, false, &ss);
+  if (trial_reuse_ok() && prob_.variant == 2) {
+    // keep the whole u series: if this trial is accepted, the forward at the same
+    // velocity (optimizer.hpp:219) adopts it instead of recomputing (forward())
+    solve_displacement_fwd(trial_prov_, trial_u_.p, true, nullptr);
+    warp_m1(trial_u_.p + prob_.nt * vec_elems(), trial_m1_.p, trial_res_.p, false, &ss);
+    trial_valid_ = true;
+  } else {
+    solve_displacement_fwd(trial_prov_, nullptr, false, bt(11));
+    warp_m1(bt(11), trial_m1_.p, trial_res_.p, false, &ss);
+  }
   const double er = reg_energy(v);
   return er + ss * cell_volume_ / prob_.sigma2;
 }

@@ -211,6 +211,13 @@ class Engine {
   DevBuf<double2> tmp_u_;     // trial u running state [2][3][Kprod]
   DevBuf<float> m1_, res_, gsw_, ugrid_;  // m1, residual [N], grad_src_warped [3][N], u(1) embed [3][N]
   DevBuf<float> trial_m1_, trial_res_;
+  // trial-state reuse (stationary SL, deformation-state): the last energy() keeps its u
+  // series; a forward() at the bitwise-same velocity adopts it
+  DevBuf<double2> trial_u_;
+  bool trial_valid_ = false;
+  bool trial_reuse_ok() const { return prob_.stationary && !prob_.rk4 && std::getenv("LDDMM_NO_TRIAL_REUSE") == nullptr; }
+  bool same_velocity(const double2* a, const double2* b);
+  void adopt_trial_provider(bool with_bwd);
   DevBuf<double2> btmp_;      // band temporaries: 12 band vectors
   DevBuf<double2> src_;       // (nt+1) band vectors (incremental sources)
   DevBuf<double2> dseries_;   // (nt+1) band vectors (hessvec du / drho series)

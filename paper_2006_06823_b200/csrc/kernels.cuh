@@ -175,6 +175,7 @@ void launch_products(int op, long long n, const float* a, const float* b, float*
 struct NodeWeights {
   float w[8];
 };
+void launch_equal_flag(long long n, const double* a, const double* b, unsigned long long* mismatch, cudaStream_t s);
 void launch_jac_batch(bool transpose, int nn, long long M, const float* derivs, const float* w,
                       long long w_node_stride, float* out, long long out_stride, NodeWeights wts, bool init,
                       cudaStream_t s);
