@@ -123,7 +123,7 @@ Engine::Engine(const Problem& p, int device) : prob_(p), device_(device) {
   ugrid_.alloc(3 * N);
   trial_m1_.alloc(N);
   trial_res_.alloc(N);
-  if (trial_reuse_ok()) trial_u_.alloc((p.nt + 1) * V);
+  if (trial_reuse_ok() && p.variant != 0) trial_u_.alloc((p.nt + 1) * V);
   I1_.alloc(N);
   I0f_.alloc(N);
   I0coef_.alloc(4 * N);  // I0 spline coefficients followed by grad I0 spline coefficients
@@ -532,7 +532,10 @@ void Engine::adopt_trial_provider(bool with_bwd) {
   swapbuf(prov_.v, trial_prov_.v);
   swapbuf(prov_.div, trial_prov_.div);
   swapbuf(prov_.dep_fwd, trial_prov_.dep_fwd);
-  swapbuf(u_, trial_u_);
+  if (prob_.variant == 0)
+    swapbuf(m_ser_, trial_mser_);  // transported image series (original)
+  else
+    swapbuf(u_, trial_u_);  // displacement series (state / deformation-state)
   prov_.cfl = trial_prov_.cfl;
   pullback_large_ = prov_.cfl * prob_.nt > 1.0;
   prov_.has_bwd = false;
@@ -859,7 +862,7 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
   // after trial_energy at the same tv_axpy result) adopts the trial's provider and u
   // series instead of recomputing them: the same kernels on the same inputs, so the
   // values are identical; only the backward departures are added.
-  const bool reuse = prob_.variant == 2 && trial_reuse_ok() && trial_valid_ && same_velocity(v, trial_prov_.v.p);
+  const bool reuse = trial_reuse_ok() && trial_valid_ && same_velocity(v, trial_prov_.v.p);
   trial_valid_ = false;
   if (reuse) {
     adopt_trial_provider(with_adjoint);
@@ -870,9 +873,9 @@ Energies Engine::forward(const double2* v, bool with_adjoint) {
   e.cfl = prov_.cfl;
   double ss = 0.0;
   if (prob_.variant == 0) {
-    ss = forward_original(with_adjoint, v);
+    ss = forward_original(with_adjoint, v, reuse);
   } else if (prob_.variant == 1) {
-    ss = forward_state(with_adjoint);
+    ss = forward_state(with_adjoint, reuse);
   } else {
     if (!reuse) solve_displacement_fwd(prov_, u_.p, true, nullptr);
     warp_m1(u_.p + prob_.nt * V, m1_.p, res_.p, with_adjoint, &ss);
@@ -899,7 +902,7 @@ double Engine::energy(const double2* v) {
   trial_valid_ = false;  // set again only when this trial completes
   provider_build(v, trial_prov_, false);
   double ss = 0.0;
-  if (trial_reuse_ok() && prob_.variant == 2) {
+  if (trial_reuse_ok()) {  // state / deformation-state variants
     // keep the whole u series: if this trial is accepted, the forward at the same
     // velocity (optimizer.hpp:219) adopts it instead of recomputing (forward())
     solve_displacement_fwd(trial_prov_, trial_u_.p, true, nullptr);

@@ -211,9 +211,9 @@ class Engine {
   DevBuf<double2> tmp_u_;     // trial u running state [2][3][Kprod]
   DevBuf<float> m1_, res_, gsw_, ugrid_;  // m1, residual [N], grad_src_warped [3][N], u(1) embed [3][N]
   DevBuf<float> trial_m1_, trial_res_;
-  // trial-state reuse (stationary SL, deformation-state): the last energy() keeps its u
-  // series; a forward() at the bitwise-same velocity adopts it
-  DevBuf<double2> trial_u_;
+  // trial-state reuse (stationary SL, all variants): the last energy() keeps its u (or
+  // image) series; a forward() at the bitwise-same velocity adopts it
+  DevBuf<double2> trial_u_, trial_mser_;
   bool trial_valid_ = false;
   bool trial_reuse_ok() const { return prob_.stationary && !prob_.rk4 && std::getenv("LDDMM_NO_TRIAL_REUSE") == nullptr; }
   bool same_velocity(const double2* a, const double2* b);
@@ -302,8 +302,8 @@ class Engine {
   void assemble_star_grad(const double2* Lam, const double2* Mser, const double2* like, double2* out);
   void grid_spline(const float* f, float* coef);
   void lambda_nodes_state(const float* lam1, double2* out_series);
-  double forward_original(bool with_adjoint, const double2* v);
-  double forward_state(bool with_adjoint);
+  double forward_original(bool with_adjoint, const double2* v, bool have_m = false);
+  double forward_state(bool with_adjoint, bool have_u = false);
   double energy_original(const double2* v);
   void hessvec_original(const double2* dv, double2* out);
   void hessvec_state(const double2* dv, double2* out);

@@ -34,6 +34,7 @@ void Engine::ensure_variant_buffers() {
     m_ser_.alloc((nt + 1) * S);
     lam_ser_.alloc((nt + 1) * S);
     dm_ser_.alloc((nt + 1) * S);
+    if (prob_.variant == 0 && trial_reuse_ok()) trial_mser_.alloc((nt + 1) * S);
   }
   if (prob_.variant == 1 && !nu_ser_.p) {
     nu_ser_.alloc((nt + 1) * V);
@@ -244,11 +245,11 @@ void Engine::lambda_nodes_state(const float* lam1, double2* out_series) {
 }
 
 // forward_original (variants.hpp:373-384); returns sum(res^2)
-double Engine::forward_original(bool with_adjoint, const double2* v) {
+double Engine::forward_original(bool with_adjoint, const double2* v, bool have_m) {
   const long long N = npts(), S = kprod();
   const int nt = prob_.nt;
   (void)v;
-  solve_image_forward(prov_, m0_.p, m_ser_.p, true, nullptr);
+  if (!have_m) solve_image_forward(prov_, m0_.p, m_ser_.p, true, nullptr);  // else adopted from the trial
   embed(m_ser_.p + nt * S, 1, m1_.p, false);
   const int g = launch_residual(N, m1_.p, I1_.p, res_.p, part_.p, stream_);
   const double ss = reduce(g, 0);
@@ -263,21 +264,29 @@ double Engine::forward_original(bool with_adjoint, const double2* v) {
 
 double Engine::energy_original(const double2* v) {
   const long long N = npts(), S = kprod();
+  trial_valid_ = false;  // set again only when this trial completes
   provider_build(v, trial_prov_, false);
-  double2* last = bt(11);
-  solve_image_forward(trial_prov_, m0_.p, nullptr, false, last);
+  const double2* last;
+  if (trial_reuse_ok()) {
+    // keep the whole image series for a forward at the same velocity (see forward())
+    solve_image_forward(trial_prov_, m0_.p, trial_mser_.p, true, nullptr);
+    last = trial_mser_.p + prob_.nt * S;
+  } else {
+    solve_image_forward(trial_prov_, m0_.p, nullptr, false, bt(11));
+    last = bt(11);
+  }
   embed(last, 1, trial_m1_.p, false);
   const int g = launch_residual(N, trial_m1_.p, I1_.p, trial_res_.p, part_.p, stream_);
   const double ss = reduce(g, 0);
-  (void)S;
+  if (trial_reuse_ok()) trial_valid_ = true;
   return reg_energy(v) + ss * cell_volume_ / prob_.sigma2;
 }
 
 // forward_state (variants.hpp:386-422); returns sum(res^2)
-double Engine::forward_state(bool with_adjoint) {
+double Engine::forward_state(bool with_adjoint, bool have_u) {
   const long long N = npts(), S = kprod(), V = vec_elems();
   const int nt = prob_.nt;
-  solve_displacement_fwd(prov_, u_.p, true, nullptr);
+  if (!have_u) solve_displacement_fwd(prov_, u_.p, true, nullptr);  // else adopted from the trial
   double ss = 0.0;
   warp_m1(u_.p + nt * V, m1_.p, res_.p, false, &ss);
   if (!with_adjoint) return ss;
