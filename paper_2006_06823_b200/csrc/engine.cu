@@ -18,6 +18,7 @@
 //  * hoisting: I0 and grad I0 spline coefficients are per-registration constants.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
@@ -217,6 +218,18 @@ void Engine::build_plan(DftPlan& p, const int* Ng, const int* K, const double* w
     p.uz_p_big = alloc(nc);
     p.uz_p_small = alloc(nc);
     launch_umma_zproj_prep(p.tz_p_big, p.tz_p_small, Nz, 2 * H, p.uz_p_big, p.uz_p_small, stream_);
+  }
+  // x stage on tcgen05 (twiddles as the canonical K-major operand) where the plan fits
+  if (!(std::getenv("LDDMM_UMMA_X") && std::getenv("LDDMM_UMMA_X")[0] == '0')) {
+    std::vector<float> tw;
+    if (umma_xstage_fits(Nx, Kx, Ny * H)) {
+      umma_xstage_twiddles_host(wx_e.data(), Nx, Kx, tw);
+      p.ux_e = (float*)upload(tw.data(), tw.size() * sizeof(float));
+    }
+    if (umma_xstage_fits(Kx, Nx, Ny * H)) {
+      umma_xstage_twiddles_host(wx_p.data(), Kx, Nx, tw);
+      p.ux_p = (float*)upload(tw.data(), tw.size() * sizeof(float));
+    }
   }
   if (umma_zembed_fits(Nz, 2 * H)) {
     const size_t nc = (size_t)umma_padded_n(Nz) * 2 * H;

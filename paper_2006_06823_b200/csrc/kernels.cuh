@@ -1,6 +1,8 @@
 // Kernel launch interfaces shared by the engine translation units.
 #pragma once
 
+#include <vector>
+
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -58,6 +60,9 @@ struct DftPlan {
   float *uz_e_big = nullptr, *uz_e_small = nullptr;
   // Tz_p in the canonical UMMA layout, K zero-padded to whole chunks (tcgen05 z-project), or null
   float *uz_p_big = nullptr, *uz_p_small = nullptr;
+  // Wx_e / Wx_p as the tcgen05 x-stage twiddle operand (umma_xstage.cu: real / imaginary x
+  // TF32 big / small, canonical K-major), or null (FFMA x stage)
+  float *ux_e = nullptr, *ux_p = nullptr;
   long long npts() const { return (long long)N[0] * N[1] * N[2]; }
   long long half() const { return (long long)K[0] * K[1] * (K[2] / 2); }
   long long kprod() const { return (long long)K[0] * K[1] * K[2]; }
@@ -79,6 +84,13 @@ void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int l
 void launch_tc3_gemm(const float* A, int lda, long long sA, const float* Bbig, const float* Bsmall, int ldb, float* C,
                      int ldc, long long sC, int M, int N, int K, int batch, cudaStream_t s);
 void launch_tf32_split(const float* in, float* big, float* small, long long n, cudaStream_t s);
+// tcgen05 3xTF32 complex x-stage GEMM (umma_xstage.cu): C[f] = W X[f], W [M][K], X [K][N],
+// C [M][N] complex; twiddle operand prepared on the host
+bool umma_xstage_fits(int M, int K, int N);
+long long umma_xstage_twiddle_floats(int M, int K);
+void umma_xstage_twiddles_host(const float2* W, int M, int K, std::vector<float>& out);
+void launch_umma_xstage(const float* tw, const float2* X, long long sX, float2* C, long long sC, int M, int N, int K,
+                        int nf, cudaStream_t s);
 // tcgen05 3xTF32 embed-z GEMM (umma_gemm.cu): C[b] = A[b] * B, A [M][K] rows, C [M][N] rows
 int umma_padded_n(int N);
 bool umma_zembed_fits(int N, int K);

@@ -526,8 +526,11 @@ static void dft_embed_xz(const DftPlan& p, int nf, const float2* E1, float2* E2,
   const int Kx = p.K[0], H = p.K[2] / 2;
   const int Nx = p.N[0], Ny = p.N[1], Nz = p.N[2];
   // X: for each f: E2[Nx x (Ny H)] = Wx[Nx x Kx] * E1[Kx x (Ny H)]
-  launch_cgemm(p.wx_e, Kx, E1, (long long)Kx * Ny * H, Ny * H, E2, (long long)Nx * Ny * H, Ny * H, Nx, Ny * H,
-               Kx, nf, s);
+  if (p.ux_e)
+    launch_umma_xstage(p.ux_e, E1, (long long)Kx * Ny * H, E2, (long long)Nx * Ny * H, Nx, Ny * H, Kx, nf, s);
+  else
+    launch_cgemm(p.wx_e, Kx, E1, (long long)Kx * Ny * H, Ny * H, E2, (long long)Nx * Ny * H, Ny * H, Nx, Ny * H,
+                 Kx, nf, s);
   // Z: for each f: out[(Nx Ny) x Nz] = E2 as float[(Nx Ny) x 2H] * Tz_e[2H x Nz]
   if (use_tensor_cores() && use_umma() && p.uz_e_big)
     launch_umma_zembed(reinterpret_cast<const float*>(E2), (long long)Nx * Ny * 2 * H, p.uz_e_big, p.uz_e_small, out,
@@ -555,8 +558,11 @@ static void dft_project_zx(const DftPlan& p, const float* f, int nf, float2* G1,
   else
     launch_sgemm(f, Nz, (long long)Nx * Ny * Nz, p.tz_p, 2 * H, reinterpret_cast<float*>(G1), 2 * H,
                  (long long)Nx * Ny * 2 * H, Nx * Ny, 2 * H, Nz, nf, s);
-  launch_cgemm(p.wx_p, Nx, G1, (long long)Nx * Ny * H, Ny * H, G2, (long long)Kx * Ny * H, Ny * H, Kx, Ny * H,
-               Nx, nf, s);
+  if (p.ux_p)
+    launch_umma_xstage(p.ux_p, G1, (long long)Nx * Ny * H, G2, (long long)Kx * Ny * H, Kx, Ny * H, Nx, nf, s);
+  else
+    launch_cgemm(p.wx_p, Nx, G1, (long long)Nx * Ny * H, Ny * H, G2, (long long)Kx * Ny * H, Ny * H, Kx, Ny * H,
+                 Nx, nf, s);
 }
 
 void dft_project(const DftPlan& p, const float* f, int nf, float2* G1, float2* G2, float2* G3, cudaStream_t s) {
