@@ -379,21 +379,21 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
   } else if (warp == 1) {
     if (lane == 0) {
       // MMA issuer
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(2 * NT >> 3) << 17) | ((128u >> 4) << 24);
       for (int s = 0; s < S; ++s) {
         const int t = s / nk, j = s % nk;
         if (j == 0 && t >= 2) mbar_wait(&acc_free[t & 1], par(t - 2, 2));
         mbar_wait(&split_done[s % NBUF], par(s, NBUF));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t acc = tmem + (uint32_t)((t & 1) * NT);
+        const uint32_t acc = tmem + (uint32_t)((t & 1) * 2 * NT);
         const uint32_t a_big = su32(ring + (s % NBUF) * CH), a_sml = su32(smallb + (s % NSB) * CH);
         const uint32_t b_off = (uint32_t)j * (ZP_KC / 4) * 128;
-        const uint32_t b_big = su32(Bb) + b_off, b_sml = su32(Bs) + b_off;
-        for (int pass = 0; pass < 3; ++pass) {
-          const uint32_t aop = pass == 0 ? a_sml : a_big, bop = pass == 1 ? b_sml : b_big;
-          for (int ks = 0; ks < ZP_KC / 8; ++ks)
-            umma_tf32(acc, umma_desc_sw128(aop + ks * 32), umma_desc(bop + ks * 2 * LBO_B, LBO_B, SBO_B), idesc,
-                      (j | pass | ks) ? 1u : 0u);
+        const uint32_t b_big = su32(Bb) + b_off;  // B_small follows as canonical rows NT .. 2 NT - 1
+        for (int ks = 0; ks < ZP_KC / 8; ++ks) {
+          const uint64_t bd = umma_desc(b_big + ks * 2 * LBO_B, LBO_B, SBO_B);
+          umma_tf32(acc, umma_desc_sw128(a_big + ks * 32), bd, idesc2, (j | ks) ? 1u : 0u);  // [Ab Bb | Ab Bs]
+          umma_tf32(acc, umma_desc_sw128(a_sml + ks * 32), bd, idesc1, 1u);                 // += As Bb
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          su32(&mma_done[s % NBUF]))
@@ -410,20 +410,23 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
     for (int t = 0; t < my_tiles; ++t) {
       mbar_wait(&acc_full[t & 1], par(t, 2));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t acc = tmem + (uint32_t)((t & 1) * NT);
+      const uint32_t acc = tmem + (uint32_t)((t & 1) * 2 * NT);
       const int m = ((int)blockIdx.x + t * (int)gridDim.x) * 128 + qd * 32 + lane;
       float* crow = C + (long long)m * NT;
 #pragma unroll
       for (int c0 = 0; c0 < NT; c0 += 16) {
-        uint32_t r[16];
+        uint32_t r[16], r2[16];
         tmem_ld16(acc + ((uint32_t)(qd * 32) << 16) + c0, r);
+        tmem_ld16(acc + ((uint32_t)(qd * 32) << 16) + NT + c0, r2);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         if (m < M) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(crow + c0 + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                                                                    __uint_as_float(r[i + 2]),
-                                                                    __uint_as_float(r[i + 3]));
+            *reinterpret_cast<float4*>(crow + c0 + i) =
+                make_float4(__uint_as_float(r[i]) + __uint_as_float(r2[i]),
+                            __uint_as_float(r[i + 1]) + __uint_as_float(r2[i + 1]),
+                            __uint_as_float(r[i + 2]) + __uint_as_float(r2[i + 2]),
+                            __uint_as_float(r[i + 3]) + __uint_as_float(r2[i + 3]));
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
