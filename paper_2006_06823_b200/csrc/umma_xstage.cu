@@ -106,13 +106,14 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
                                                                     const float* __restrict__ Tw,
                                                                     float* __restrict__ C, long long sC, int M,
                                                                     int N2, int Kpad, int Mpad, int nf, int NG,
-                                                                    int G, int NACC) {
+                                                                    int G, int NACC, int UC) {
   constexpr uint32_t LBO_B = 128;
   const uint32_t SBO_B = (uint32_t)(Kpad / 4) * 128;
-  // TMEM: NACC buffers x nk k-chunks x (P, Q) x NG columns.  Every k chunk accumulates into
-  // its own (P, Q) pair and the epilogue adds the chunks in fp32: the tensor core's fp32
-  // accumulation, 180 terms deep at the config-2 project, cost 2x the error of the FFMA
-  // stage and broke the SURVEY 8(c) energy tolerance; 32 terms deep it does not.
+  // TMEM: NACC buffers of UC columns per accumulator unit: with several k chunks one (P, Q)
+  // pair per chunk (big-twiddle products) and one for the small-twiddle corrections, added
+  // by the epilogue in fp32; with one chunk a single (P, Q) pair.  The tensor core's fp32 accumulation, 180 terms deep at the
+  // config-2 project, cost 2x the error of the FFMA stage and broke the SURVEY 8(c) energy
+  // tolerance; 32 terms deep it does not.
   extern __shared__ __align__(1024) float sm[];
   float* ring = sm;                        // NBUF raw chunks (TMA destination, [4 boxes][KC][32])
   float* opb = ring + XS_NBUF * XS_CH;     // NSB x (big, small) canonical K-major chunks
@@ -185,10 +186,13 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // MMA issuer: per chunk, per m-group g: P += X^T Wr^T, Q += X^T Wi^T (3 passes each)
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NG >> 3) << 17) | ((128u >> 4) << 24);
+      // MMA issuer, per chunk and m-group g (twiddle rows of the group: [Wr_big; Wi_big;
+      // Wr_small; Wi_small], NG each, consecutive canonical rows), each N = 2 NG MMA
+      // producing [P | Q]: X_big [Wr_b; Wi_b] -> big_j (chunk j), X_big [Wr_s; Wi_s] -> corr,
+      // X_small [Wr_b; Wi_b] -> big_j.  One chunk (embed, K = 32): corr = big_0.
+      const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(2 * NG >> 3) << 17) | ((128u >> 4) << 24);
       constexpr uint32_t SBO_A = (XS_KC / 4) * 128;
-      const uint32_t tw0 = xs_su32(tw), twa = (uint32_t)Mpad * Kpad * 4;  // bytes per twiddle array
+      const uint32_t tw0 = xs_su32(tw);
       for (int s = 0; s < S; ++s) {
         const int t = s / nk, j = s % nk;
         xs_wait(&ready[s % XS_NSB], par(s, XS_NSB));
@@ -198,19 +202,18 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
           const int u = t * G + g;  // accumulator unit
           if (j == 0 && u >= NACC) xs_wait(&acc_free[u % NACC], par(u - NACC, NACC));
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          const uint32_t accP = tmem + (uint32_t)(((u % NACC) * nk + j) * 2 * NG), accQ = accP + (uint32_t)NG;
-          // twiddle rows g NG .. (8-row groups SBO_B apart), k chunk j (XS_KC / 4 core matrices of 128 B)
-          const uint32_t b_off = (uint32_t)(g * NG / 8) * SBO_B + (uint32_t)j * (XS_KC / 4) * 128;
-          for (int pass = 0; pass < 3; ++pass) {
-            const uint32_t aop = pass == 0 ? a_sml : a_big;
-            const uint32_t wr = tw0 + (pass == 1 ? twa : 0u) + b_off;      // real big / small
-            const uint32_t wi = tw0 + 2 * twa + (pass == 1 ? twa : 0u) + b_off;  // imag big / small
-            for (int ks = 0; ks < XS_KC / 8; ++ks) {
-              const uint64_t ad = xs_desc_k(aop + ks * 2 * LBO_B, LBO_B, SBO_A);
-              const uint32_t acc = (pass | ks) ? 1u : 0u;
-              xs_mma(accP, ad, xs_desc_k(wr + ks * 2 * LBO_B, LBO_B, SBO_B), idesc, acc);
-              xs_mma(accQ, ad, xs_desc_k(wi + ks * 2 * LBO_B, LBO_B, SBO_B), idesc, acc);
-            }
+          const uint32_t ub = tmem + (uint32_t)((u % NACC) * UC);
+          const uint32_t big = ub + (uint32_t)(j * 2 * NG), corr = nk > 1 ? ub + (uint32_t)(nk * 2 * NG) : big;
+          // twiddle rows g 4 NG .. (8-row groups SBO_B apart), k chunk j (XS_KC / 4 core matrices of 128 B)
+          const uint32_t wb = tw0 + (uint32_t)(g * 4 * NG / 8) * SBO_B + (uint32_t)j * (XS_KC / 4) * 128;
+          const uint32_t ws = wb + (uint32_t)(2 * NG / 8) * SBO_B;
+          for (int ks = 0; ks < XS_KC / 8; ++ks) {
+            const uint64_t adb = xs_desc_k(a_big + ks * 2 * LBO_B, LBO_B, SBO_A);
+            const uint64_t ads = xs_desc_k(a_sml + ks * 2 * LBO_B, LBO_B, SBO_A);
+            const uint64_t bdb = xs_desc_k(wb + ks * 2 * LBO_B, LBO_B, SBO_B);
+            xs_mma(big, adb, bdb, idesc2, ks ? 1u : 0u);
+            xs_mma(corr, adb, xs_desc_k(ws + ks * 2 * LBO_B, LBO_B, SBO_B), idesc2, (nk == 1 || j | ks) ? 1u : 0u);
+            xs_mma(big, ads, bdb, idesc2, 1u);
           }
           if (j == nk - 1)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -236,21 +239,23 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
         const int u = t * G + g;
         xs_wait(&acc_full[u % NACC], par(u, NACC));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t acc0 = tmem + (uint32_t)((u % NACC) * nk * 2 * NG) + ((uint32_t)(qd * 32) << 16);
+        const uint32_t ub = tmem + (uint32_t)((u % NACC) * UC) + ((uint32_t)(qd * 32) << 16);
         for (int c0 = 16 * part; c0 < NG; c0 += 16 * EW) {
           float ps[16], qs[16];
           {
+            // corrections (several chunks) or the single chunk's accumulator
             uint32_t p[16], q[16];
-            xs_ld16(acc0 + c0, p);
-            xs_ld16(acc0 + (uint32_t)NG + c0, q);
+            const uint32_t c = nk > 1 ? (uint32_t)(nk * 2 * NG) : 0u;
+            xs_ld16(ub + c + c0, p);
+            xs_ld16(ub + c + (uint32_t)NG + c0, q);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 16; ++i) ps[i] = __uint_as_float(p[i]), qs[i] = __uint_as_float(q[i]);
           }
-          for (int j = 1; j < nk; ++j) {  // k chunks summed in fp32
+          for (int j = 0; j < (nk > 1 ? nk : 0); ++j) {  // k chunks summed in fp32
             uint32_t p[16], q[16];
-            xs_ld16(acc0 + (uint32_t)(j * 2 * NG) + c0, p);
-            xs_ld16(acc0 + (uint32_t)(j * 2 * NG + NG) + c0, q);
+            xs_ld16(ub + (uint32_t)(j * 2 * NG) + c0, p);
+            xs_ld16(ub + (uint32_t)(j * 2 * NG + NG) + c0, q);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 16; ++i) ps[i] += __uint_as_float(p[i]), qs[i] += __uint_as_float(q[i]);
@@ -331,8 +336,25 @@ PFN_cuTensorMapEncodeTiled_v12000 xs_encoder() {
   return fn;
 }
 
-int xs_mpad(int M) { return M <= 128 ? (M + 15) / 16 * 16 : (M + 31) / 32 * 32; }
+// output rows in G groups of NG (a multiple of 16, at most 128: 2 NG <= 256 = one MMA's N)
+void xs_groups(int M, int& G, int& NG) {
+  const int Mp = (M + 15) / 16 * 16;
+  G = (Mp + 127) / 128;
+  NG = ((Mp + G - 1) / G + 15) / 16 * 16;
+}
+int xs_mpad(int M) {
+  int G, NG;
+  xs_groups(M, G, NG);
+  return G * NG;
+}
 int xs_kpad(int K) { return (K + XS_KC - 1) / XS_KC * XS_KC; }
+
+// TMEM columns of one accumulator unit: (P, Q) per k chunk plus the corrections, or one
+// (P, Q) pair when there is a single chunk
+int xs_ucols(int K, int NG) {
+  const int nk = xs_kpad(K) / XS_KC;
+  return (nk > 1 ? nk + 1 : 1) * 2 * NG;
+}
 
 size_t xs_smem(int M, int K) {
   return ((size_t)(XS_NBUF + 2 * XS_NSB) * XS_CH + (size_t)4 * xs_mpad(M) * xs_kpad(K)) * sizeof(float) + 1024;
@@ -355,28 +377,32 @@ int xs_canon(int row, int k, int Kpad) { return ((row >> 3) * (Kpad / 4) * 128 +
 
 bool umma_xstage_fits(int M, int K, int N) {
   // M <= 256 output rows (MMA N = one or two groups of <= 128), 16-byte rows of X for the TMA
-  const int Mpad = xs_mpad(M), NG = Mpad <= 128 ? Mpad : Mpad / 2;
+  int G, NG;
+  xs_groups(M, G, NG);
   return M >= 1 && M <= 256 && K >= 1 && (2LL * N * 4) % 16 == 0 && xs_smem(M, K) <= XS_SMEM_MAX &&
-         (xs_kpad(K) / XS_KC) * 2 * NG <= 512 && xs_encoder() != nullptr;
+         xs_ucols(K, NG) <= 512 && xs_encoder() != nullptr;
 }
 
 long long umma_xstage_twiddle_floats(int M, int K) { return 4LL * xs_mpad(M) * xs_kpad(K); }
 
-// W [M][K] complex (row-major, host) -> 4 canonical arrays (Re big, Re small, Im big, Im small)
+// W [M][K] complex (row-major, host) -> the canonical K-major twiddle operand: per output
+// row group g (NG rows), rows [Re big; Im big; Re small; Im small], NG each
 void umma_xstage_twiddles_host(const float2* W, int M, int K, std::vector<float>& out) {
-  const int Mpad = xs_mpad(M), Kpad = xs_kpad(K);
-  const size_t A = (size_t)Mpad * Kpad;
-  out.assign(4 * A, 0.f);
-  for (int m = 0; m < M; ++m)
+  int G, NG;
+  xs_groups(M, G, NG);
+  const int Kpad = xs_kpad(K);
+  out.assign((size_t)4 * G * NG * Kpad, 0.f);
+  for (int m = 0; m < M; ++m) {
+    const int g = m / NG, ml = m - g * NG, r0 = g * 4 * NG + ml;
     for (int k = 0; k < K; ++k) {
       const float2 w = W[(size_t)m * K + k];
-      const int o = xs_canon(m, k, Kpad);
       const float rb = xs_tf32(w.x), ib = xs_tf32(w.y);
-      out[o] = rb;
-      out[A + o] = xs_tf32(w.x - rb);
-      out[2 * A + o] = ib;
-      out[3 * A + o] = xs_tf32(w.y - ib);
+      out[xs_canon(r0, k, Kpad)] = rb;
+      out[xs_canon(r0 + NG, k, Kpad)] = ib;
+      out[xs_canon(r0 + 2 * NG, k, Kpad)] = xs_tf32(w.x - rb);
+      out[xs_canon(r0 + 3 * NG, k, Kpad)] = xs_tf32(w.y - ib);
     }
+  }
 }
 
 // C[f][m][n] = sum_k W[m][k] X[f][k][n] (complex): X [nf][K][N] complex (field stride
@@ -393,13 +419,14 @@ void launch_umma_xstage(const float* tw, const float2* X, long long sX, float2* 
                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw EngineError(3, "umma x-stage: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  const int G = Mpad <= 128 ? 1 : 2, NG = Mpad / G;
+  int G, NG;
+  xs_groups(M, G, NG);
   const int T = nf * ((N2 + 127) / 128);
   const int grid = std::min(kSMs, T);
   const size_t smem = xs_smem(M, K);
-  // (P, Q) pairs per k chunk, double-buffered when they fit the 512 TMEM columns
-  const int nk = Kpad / XS_KC;
-  const int NACC = 2 * nk * 2 * NG <= 512 ? 2 : 1;
+  // accumulator units double-buffered when they fit the 512 TMEM columns
+  const int UC = xs_ucols(K, NG);
+  const int NACC = 2 * UC <= 512 ? 2 : 1;
   auto go = [&](auto kern, int slot) {
     static bool set[64][4] = {};
     int dev = 0;
@@ -409,9 +436,9 @@ void launch_umma_xstage(const float* tw, const float2* X, long long sX, float2* 
       set[dev & 63][slot] = true;
     }
     pdl_launch(kern, grid, XS_THREADS, smem, s, tm, tw, reinterpret_cast<float*>(C), 2 * sC, M, N2, Kpad, Mpad, nf,
-               NG, G, NACC);
+               NG, G, NACC, UC);
   };
-  const int cols = NACC * nk * 2 * NG;
+  const int cols = NACC * UC;
   if (cols <= 64)
     go(umma_xstage_kernel<64>, 0);
   else if (cols <= 128)
