@@ -407,7 +407,11 @@ def main():
                  "mode": "fixed work: grad_tol = energy_tol = step_tol = pcg_tol = 0, max_iter 10, pcg 5 "
                          "(test_optimizer.cpp:197-207)", "steps": len(f_ms),
                  "gn_iterations": fres.iterations, "hessvecs": fres.hessvecs, "trials": fres.trials,
-                 "stop": fres.stop}
+                 "stop": fres.stop,
+                 # with every tolerance 0 the solve runs until the Armijo search fails at the
+                 # fp noise floor, a point that moves with rounding: the per-iteration figure
+                 # is the comparable one
+                 "s_per_gn_iteration": max_over_ranks(float(np.mean(f_ms))) / 1000.0 / max(1, fres.iterations)}
 
     e2e = None
     if not args.no_e2e:
