@@ -342,87 +342,142 @@ __device__ __forceinline__ void fin_pair(const FinCtx& fc, int f, int fx, int fy
 // staged (bitwise the values band_prep_kernel would have written).
 // MODE 2 (FIN): the y-project with the band finalize fused in — the batch's outputs
 // go straight to the fp64 band fields (fin_pair) instead of G3.
+//
+// Work split (cgemm_split, a function of the shape only, so every MODE of a shape sums
+// in the same order): a batch item spans MS CTAs (rows [ms mrows, (ms+1) mrows)), and
+// with a long K (the y-project, K = Ny) each 2 x 2 output tile is summed by KS threads
+// over K slices, combined through shared memory in slice order — one CTA per batch
+// item with 128 busy threads left 52 SMs idle and ran K = 210 serial FMA chains.
+struct CgemmSplit {
+  int MS, KS, mrows;
+};
+
+static CgemmSplit cgemm_split(int M, int N, int K, int batch) {
+  CgemmSplit sp;
+  sp.MS = batch < 2 * kSMs && M >= 8 ? 2 : 1;
+  sp.mrows = ((M + sp.MS - 1) / sp.MS + 1) & ~1;
+  const int tiles = (sp.mrows / 2) * ((N + 1) / 2);
+  sp.KS = 1;
+  if (K > 64)
+    while (sp.KS < 8 && tiles * sp.KS * 2 <= 256) sp.KS *= 2;
+  return sp;
+}
+
 template <int MODE>
 __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restrict__ A, int lda,
                                                          const float2* __restrict__ B, long long sB, int ldb,
                                                          float2* __restrict__ C, long long sC, int ldc, int M, int N,
-                                                         int K, int batch, const __grid_constant__ PrepCtx pc,
+                                                         int K, int batch, int MS, int KS, int mrows,
+                                                         const __grid_constant__ PrepCtx pc,
                                                          const __grid_constant__ FinCtx fc) {
   constexpr bool PREP = MODE == 1, FIN = MODE == 2;
   extern __shared__ float2 sm2[];
   const int KP = K + 1;  // padded A row (bank spread across rows)
+  const int b = blockIdx.x / MS, ms = blockIdx.x - b * MS;
+  const int m_lo = ms * mrows, mh = min(M, m_lo + mrows) - m_lo;  // this CTA's rows
   float2* As = sm2;
-  float2* Bs = sm2 + (long long)M * KP;
+  float2* Bs = sm2 + (long long)mrows * KP;
+  float4* red = reinterpret_cast<float4*>(Bs + (long long)K * N);  // KS > 1: [KS][tiles] x 2 float4
   // cp.async (8-byte) copies: every element in flight at once, no register round trip.
   // A is a twiddle table (constant): staged before the PDL wait, overlapping the
   // preceding kernel's tail.
-  for (int e = threadIdx.x; e < M * K; e += blockDim.x) {
+  for (int e = threadIdx.x; e < mh * K; e += blockDim.x) {
     const int m = e / K, k = e - (e / K) * K;
-    cp_async8_f2(As + m * KP + k, A + (long long)m * lda + k);
+    cp_async8_f2(As + m * KP + k, A + (long long)(m_lo + m) * lda + k);
   }
   pdl_wait();
   pdl_trigger();
-  const int tn = (N + 1) / 2, tiles = ((M + 1) / 2) * tn;
-  for (int b = blockIdx.x; b < batch; b += gridDim.x) {
-    __syncthreads();
-    if (PREP) {
-      const int f = b / pc.Kx, fx = b - f * pc.Kx;
-      for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
-        const int k = e / N, n = e - (e / N) * N;
-        Bs[e] = prep_value(pc.a, f, fx, k, n, pc.Kx, pc.Ky, pc.Kz, pc.Nx, pc.Ny, pc.Nz, pc.wx, pc.wy, pc.wz);
-      }
-    } else {
-      const float2* Bb = B + b * sB;
-      for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
-        const int k = e / N, n = e - (e / N) * N;
-        cp_async8_f2(Bs + e, Bb + (long long)k * ldb + n);
-      }
+  if (mh <= 0) return;
+  const int tn = (N + 1) / 2, tiles = ((mh + 1) / 2) * tn;
+  if (PREP) {
+    const int f = b / pc.Kx, fx = b - f * pc.Kx;
+    for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+      const int k = e / N, n = e - (e / N) * N;
+      Bs[e] = prep_value(pc.a, f, fx, k, n, pc.Kx, pc.Ky, pc.Kz, pc.Nx, pc.Ny, pc.Nz, pc.wx, pc.wy, pc.wz);
     }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
-    float2* Cb = C + b * sC;
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-      const int m0 = (t / tn) * 2, n0 = (t - (t / tn) * tn) * 2;
-      const int m1 = min(m0 + 1, M - 1), n1 = min(n0 + 1, N - 1);
-      float2 c00 = make_float2(0.f, 0.f), c01 = c00, c10 = c00, c11 = c00;
-      const float2* a0p = As + m0 * KP;
-      const float2* a1p = As + m1 * KP;
-#pragma unroll 4
-      for (int k = 0; k < K; ++k) {
-        const float2 a0 = a0p[k], a1 = a1p[k];
-        const float2 b0 = Bs[k * N + n0], b1 = Bs[k * N + n1];
-        c00.x = fmaf(a0.x, b0.x, fmaf(-a0.y, b0.y, c00.x));
-        c00.y = fmaf(a0.x, b0.y, fmaf(a0.y, b0.x, c00.y));
-        c01.x = fmaf(a0.x, b1.x, fmaf(-a0.y, b1.y, c01.x));
-        c01.y = fmaf(a0.x, b1.y, fmaf(a0.y, b1.x, c01.y));
-        c10.x = fmaf(a1.x, b0.x, fmaf(-a1.y, b0.y, c10.x));
-        c10.y = fmaf(a1.x, b0.y, fmaf(a1.y, b0.x, c10.y));
-        c11.x = fmaf(a1.x, b1.x, fmaf(-a1.y, b1.y, c11.x));
-        c11.y = fmaf(a1.x, b1.y, fmaf(a1.y, b1.x, c11.y));
-      }
-      if (FIN) {
-        const int f = b / fc.Kx, fx = b - f * fc.Kx;
-        fin_pair(fc, f, fx, m0, n0, c00);
-        if (n0 + 1 < N) fin_pair(fc, f, fx, m0, n0 + 1, c01);
-        if (m0 + 1 < M) {
-          fin_pair(fc, f, fx, m0 + 1, n0, c10);
-          if (n0 + 1 < N) fin_pair(fc, f, fx, m0 + 1, n0 + 1, c11);
-        }
-      } else {
-        Cb[(long long)m0 * ldc + n0] = c00;
-        if (n0 + 1 < N) Cb[(long long)m0 * ldc + n0 + 1] = c01;
-        if (m0 + 1 < M) {
-          Cb[(long long)(m0 + 1) * ldc + n0] = c10;
-          if (n0 + 1 < N) Cb[(long long)(m0 + 1) * ldc + n0 + 1] = c11;
-        }
-      }
-    }
-    if (FIN) {
-      // the kz = Kz/2 plane (zero projection) of this batch's rows
-      const int f = b / fc.Kx, fx = b - f * fc.Kx;
-      for (int fy = threadIdx.x; fy < M; fy += blockDim.x) fin_store(fc, f, fx, fy, fc.Kz / 2, 0.0, 0.0);
+  } else {
+    const float2* Bb = B + b * sB;
+    for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+      const int k = e / N, n = e - (e / N) * N;
+      cp_async8_f2(Bs + e, Bb + (long long)k * ldb + n);
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  float2* Cb = C + b * sC;
+  auto emit = [&](int m0, int n0, float2 c00, float2 c01, float2 c10, float2 c11) {
+    const int M0 = m_lo + m0;
+    if (FIN) {
+      const int f = b / fc.Kx, fx = b - f * fc.Kx;
+      fin_pair(fc, f, fx, M0, n0, c00);
+      if (n0 + 1 < N) fin_pair(fc, f, fx, M0, n0 + 1, c01);
+      if (m0 + 1 < mh) {
+        fin_pair(fc, f, fx, M0 + 1, n0, c10);
+        if (n0 + 1 < N) fin_pair(fc, f, fx, M0 + 1, n0 + 1, c11);
+      }
+    } else {
+      Cb[(long long)M0 * ldc + n0] = c00;
+      if (n0 + 1 < N) Cb[(long long)M0 * ldc + n0 + 1] = c01;
+      if (m0 + 1 < mh) {
+        Cb[(long long)(M0 + 1) * ldc + n0] = c10;
+        if (n0 + 1 < N) Cb[(long long)(M0 + 1) * ldc + n0 + 1] = c11;
+      }
+    }
+  };
+  const int kslice = (K + KS - 1) / KS;
+  for (int it = threadIdx.x; it < tiles * KS; it += blockDim.x) {
+    const int t = it % tiles, ks = it / tiles;
+    const int m0 = (t / tn) * 2, n0 = (t - (t / tn) * tn) * 2;
+    const int m1 = min(m0 + 1, mh - 1), n1 = min(n0 + 1, N - 1);
+    float2 c00 = make_float2(0.f, 0.f), c01 = c00, c10 = c00, c11 = c00;
+    const float2* a0p = As + m0 * KP;
+    const float2* a1p = As + m1 * KP;
+    const int k_lo = ks * kslice, k_hi = min(K, k_lo + kslice);
+#pragma unroll 4
+    for (int k = k_lo; k < k_hi; ++k) {
+      const float2 a0 = a0p[k], a1 = a1p[k];
+      const float2 b0 = Bs[k * N + n0], b1 = Bs[k * N + n1];
+      c00.x = fmaf(a0.x, b0.x, fmaf(-a0.y, b0.y, c00.x));
+      c00.y = fmaf(a0.x, b0.y, fmaf(a0.y, b0.x, c00.y));
+      c01.x = fmaf(a0.x, b1.x, fmaf(-a0.y, b1.y, c01.x));
+      c01.y = fmaf(a0.x, b1.y, fmaf(a0.y, b1.x, c01.y));
+      c10.x = fmaf(a1.x, b0.x, fmaf(-a1.y, b0.y, c10.x));
+      c10.y = fmaf(a1.x, b0.y, fmaf(a1.y, b0.x, c10.y));
+      c11.x = fmaf(a1.x, b1.x, fmaf(-a1.y, b1.y, c11.x));
+      c11.y = fmaf(a1.x, b1.y, fmaf(a1.y, b1.x, c11.y));
+    }
+    if (KS == 1) {
+      emit(m0, n0, c00, c01, c10, c11);
+    } else {
+      red[(ks * tiles + t) * 2] = make_float4(c00.x, c00.y, c01.x, c01.y);
+      red[(ks * tiles + t) * 2 + 1] = make_float4(c10.x, c10.y, c11.x, c11.y);
+    }
+  }
+  if (KS > 1) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+      float4 p = red[t * 2], q = red[t * 2 + 1];
+      for (int ks = 1; ks < KS; ++ks) {
+        const float4 p2 = red[(ks * tiles + t) * 2], q2 = red[(ks * tiles + t) * 2 + 1];
+        p.x += p2.x, p.y += p2.y, p.z += p2.z, p.w += p2.w;
+        q.x += q2.x, q.y += q2.y, q.z += q2.z, q.w += q2.w;
+      }
+      const int m0 = (t / tn) * 2, n0 = (t - (t / tn) * tn) * 2;
+      emit(m0, n0, make_float2(p.x, p.y), make_float2(p.z, p.w), make_float2(q.x, q.y), make_float2(q.z, q.w));
+    }
+  }
+  if (FIN && ms == 0) {
+    // the kz = Kz/2 plane (zero projection) of this batch's rows
+    const int f = b / fc.Kx, fx = b - f * fc.Kx;
+    for (int fy = threadIdx.x; fy < M; fy += blockDim.x) fin_store(fc, f, fx, fy, fc.Kz / 2, 0.0, 0.0);
+  }
+}
+
+static size_t cgemm_smem_bytes(int M, int N, int K, int batch) {
+  const CgemmSplit sp = cgemm_split(M, N, K, batch);
+  const int tiles = (sp.mrows / 2) * ((N + 1) / 2);
+  return ((size_t)sp.mrows * (K + 1) + (size_t)K * N) * sizeof(float2) +
+         (sp.KS > 1 ? (size_t)sp.KS * tiles * 2 * sizeof(float4) : 0);
 }
 
 static bool cgemm_smem_fits(int M, int N, int K) {
@@ -433,7 +488,8 @@ template <int MODE>
 static void launch_cgemm_smem(const float2* A, int lda, const float2* B, long long sB, int ldb, float2* C,
                               long long sC, int ldc, int M, int N, int K, int batch, const PrepCtx& pc,
                               const FinCtx& fc, cudaStream_t s) {
-  const size_t smem = ((size_t)M * (K + 1) + (size_t)K * N) * sizeof(float2);
+  const CgemmSplit sp = cgemm_split(M, N, K, batch);
+  const size_t smem = cgemm_smem_bytes(M, N, K, batch);
   static bool attr_set[64] = {false};
   int dev = 0;
   LDDMM_CUDA(cudaGetDevice(&dev));
@@ -442,7 +498,8 @@ static void launch_cgemm_smem(const float2* A, int lda, const float2* B, long lo
         cudaFuncSetAttribute(cgemm_smem_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set[dev & 63] = true;
   }
-  pdl_launch(cgemm_smem_kernel<MODE>, batch, 256, smem, s, A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch, pc, fc);
+  pdl_launch(cgemm_smem_kernel<MODE>, batch * sp.MS, 256, smem, s, A, lda, B, sB, ldb, C, sC, ldc, M, N, K, batch,
+             sp.MS, sp.KS, sp.mrows, pc, fc);
   LDDMM_LAUNCH_CHECK();
 }
 
