@@ -379,7 +379,8 @@ bool umma_xstage_fits(int M, int K, int N) {
   // M <= 256 output rows (MMA N = one or two groups of <= 128), 16-byte rows of X for the TMA
   int G, NG;
   xs_groups(M, G, NG);
-  return M >= 1 && M <= 256 && K >= 1 && (2LL * N * 4) % 16 == 0 && xs_smem(M, K) <= XS_SMEM_MAX &&
+  // TMA: 16-byte row pitch (2N floats) and field stride (K N complex, the callers' layouts)
+  return M >= 1 && M <= 256 && K >= 1 && N % 2 == 0 && (1LL * K * N) % 2 == 0 && xs_smem(M, K) <= XS_SMEM_MAX &&
          xs_ucols(K, NG) <= 512 && xs_encoder() != nullptr;
 }
 
