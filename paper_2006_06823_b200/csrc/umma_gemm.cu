@@ -444,16 +444,15 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
       for (int u = 0; u < CH / 4 / 256; ++u) {
         const int e = st + u * 256;
         const float4 a = reinterpret_cast<const float4*>(big)[e];
-        // round-to-nearest TF32 parts (big exact in TF32; a - big exact in fp32, then rounded)
+        // TF32 parts: big = round-to-nearest TF32 (exact in TF32), small = a - big (exact in
+        // fp32; the tensor core reads its leading 19 bits)
         float4 bg;
         bg.x = __uint_as_float(tf32_bits(a.x));
         bg.y = __uint_as_float(tf32_bits(a.y));
         bg.z = __uint_as_float(tf32_bits(a.z));
         bg.w = __uint_as_float(tf32_bits(a.w));
         reinterpret_cast<float4*>(big)[e] = bg;
-        reinterpret_cast<float4*>(sml)[e] =
-            make_float4(__uint_as_float(tf32_bits(a.x - bg.x)), __uint_as_float(tf32_bits(a.y - bg.y)),
-                        __uint_as_float(tf32_bits(a.z - bg.z)), __uint_as_float(tf32_bits(a.w - bg.w)));
+        reinterpret_cast<float4*>(sml)[e] = make_float4(a.x - bg.x, a.y - bg.y, a.z - bg.z, a.w - bg.w);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive(&split_done[s % NBUF]);

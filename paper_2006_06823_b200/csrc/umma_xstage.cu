@@ -300,12 +300,12 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
         float a[4], bg[4], sl[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = src[i * 32];
-        // round-to-nearest TF32 parts (big exact in TF32, a - big exact in fp32, then rounded):
-        // half the error of truncated parts, which the config-2 energy tolerance needs
+        // big = round-to-nearest TF32 (exact in TF32; half the error of a truncated big part,
+        // which the config-2 energy tolerance needs), small = a - big (exact in fp32)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           bg[i] = xs_tf32_rna(a[i]);
-          sl[i] = xs_tf32_rna(a[i] - bg[i]);
+          sl[i] = a[i] - bg[i];
         }
         const int off = ((nc >> 3) * (XS_KC / 4) * 128 + kq * 128 + (nc & 7) * 16) / 4;
         *reinterpret_cast<float4*>(big + off) = make_float4(bg[0], bg[1], bg[2], bg[3]);
