@@ -392,8 +392,10 @@ __global__ __launch_bounds__(ZP_THREADS, 1) void umma_zproject_kernel(const __gr
         const uint32_t b_big = su32(Bb) + b_off;  // B_small follows as canonical rows NT .. 2 NT - 1
         for (int ks = 0; ks < ZP_KC / 8; ++ks) {
           const uint64_t bd = umma_desc(b_big + ks * 2 * LBO_B, LBO_B, SBO_B);
+#ifndef ZP_NOMMA  // lab: the pipeline without the MMAs (tools/lab/build_variant.sh)
           umma_tf32(acc, umma_desc_sw128(a_big + ks * 32), bd, idesc2, (j | ks) ? 1u : 0u);  // [Ab Bb | Ab Bs]
           umma_tf32(acc, umma_desc_sw128(a_sml + ks * 32), bd, idesc1, 1u);                 // += As Bb
+#endif
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          su32(&mma_done[s % NBUF]))
