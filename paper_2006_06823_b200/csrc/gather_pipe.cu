@@ -255,14 +255,14 @@ __device__ __forceinline__ void gp_item(const NodeD& r0, const NodeD& r1, const 
 }
 
 // One-row item: row j x group g (5 x 5 source rows; gw_item's arithmetic).
-template <int NC, int P>
+template <int NC, int P, bool UNIT>
 __device__ __forceinline__ void gp_item1(const NodeD& r0, const float* const (&pl)[5], int CV, int offA, int offB,
                                          const float* __restrict__ coef, const float* __restrict__ disp,
                                          float* __restrict__ out, long long N, int c0, int i, int j, int g, int Nx,
                                          int Ny, int Nz, float3 sc) {
   const long long rowp0 = ((long long)i * Ny + j) * Nz;
   const int zA = g == 0 ? Nz - 2 : 4 * g - 2, zB = 4 * g;
-  const NodeD d0 = gp_scaled(r0, sc);
+  const NodeD d0 = UNIT ? r0 : gp_scaled(r0, sc);  // unit scale (SL steps): x * 1 is exact
   if (!gp_regime(d0)) {
 #pragma unroll 1
     for (int m = 0; m < 4; ++m) {
@@ -308,7 +308,7 @@ __device__ __forceinline__ void gp_item1(const NodeD& r0, const float* const (&p
 }
 
 // tm_box: box {P, R, 1} (tiles whose staged y rows do not wrap); tm_row: box {P, 2, 1}.
-template <int FG, int P>
+template <int FG, int P, bool UNIT>
 __global__ __launch_bounds__(GP_NTH, 1) void gather_pipe_kernel(const __grid_constant__ CUtensorMap tm_box,
                                                                 const __grid_constant__ CUtensorMap tm_row,
                                                                 const float* __restrict__ coef, int F,
@@ -396,55 +396,85 @@ __global__ __launch_bounds__(GP_NTH, 1) void gather_pipe_kernel(const __grid_con
         ++released;
       }
     };
-    // item q -> (row r, pair ry2, group g); the displacements of the warp's next item
-    // are loaded while the current one computes (the weights need them first thing)
-    auto decode = [&](int q, int& r, int& ry2, int& g) {
-      r = q / IPR;
-      const int loc = q - r * IPR;
-      ry2 = loc / G;
-      g = loc - ry2 * G;
+    // item q -> (row r, y row ry2, group g), carried incrementally (no integer divisions
+    // on the path): a lane's items advance by STEP = GP_CW * 32 per iteration.  The
+    // displacements of the warp's next item are loaded while the current one computes
+    // (the weights need them first thing).
+    constexpr int STEP = GP_CW * 32;
+    struct Pos {
+      int r, ry, g, slot;  // slot = ring slot of plane base + r (the item's first source plane)
     };
-    auto load = [&](int q, NodeD& d0, NodeD& d1) {
+    const int TYI = TY / GP_ROWS;  // item rows per tile row
+    const int step_ry = STEP / G, step_g = STEP - step_ry * G;
+    auto advance = [&](Pos& p) {
+      p.g += step_g;
+      p.ry += step_ry;
+      if (p.g >= G) {
+        p.g -= G;
+        ++p.ry;
+      }
+      while (p.ry >= TYI) {
+        p.ry -= TYI;
+        ++p.r;
+        p.slot = p.slot + 1 == GP_RING ? 0 : p.slot + 1;
+      }
+    };
+    auto load = [&](int q, const Pos& p, NodeD& d0, NodeD& d1) {
       if (q < total) {
-        int r, ry2, g;
-        decode(q, r, ry2, g);
-        const int j = min(y0 + GP_ROWS * ry2, Ny - GP_ROWS);
-        const long long rowp0 = ((long long)(x0 + r) * Ny + j) * Nz;
-        const int zA = g == 0 ? Nz - 2 : 4 * g - 2, zB = 4 * g;
+        const int j = min(y0 + GP_ROWS * p.ry, Ny - GP_ROWS);
+        const long long rowp0 = ((long long)(x0 + p.r) * Ny + j) * Nz;
+        const int zA = p.g == 0 ? Nz - 2 : 4 * p.g - 2, zB = 4 * p.g;
         gp_load_disp(disp, N, rowp0, zA, zB, d0);
         if (GP_ROWS == 2) gp_load_disp(disp, N, rowp0 + Nz, zA, zB, d1);
       }
     };
+    Pos cur;
+    {
+      const int q = cw * 32 + lane;  // the one division per lane and pass
+      cur.r = q / IPR;
+      const int loc = q - cur.r * IPR;
+      cur.ry = loc / G;
+      cur.g = loc - cur.ry * G;
+      cur.slot = (base + cur.r) % GP_RING;
+    }
+    Pos nxt = cur;
+    advance(nxt);
     NodeD n0, n1;
 #if GP_PREFETCH
-    load(cw * 32 + lane, n0, n1);
+    load(cw * 32 + lane, cur, n0, n1);
 #endif
     for (int q0 = cw * 32; q0 < total; q0 += GP_CW * 32) {
-      const int r_lo = q0 / IPR, r_hi = min(q0 + 31, total - 1) / IPR;
+      const int r_lo = __shfl_sync(0xffffffffu, cur.r, 0);
+      const int r_hi = q0 + 31 < total ? __shfl_sync(0xffffffffu, cur.r, 31) : nx - 1;
       release_below(r_lo);
       wait_to(r_hi + 4);
       const int q = q0 + lane;
 #if GP_PREFETCH
       const NodeD c0d = n0, c1d = n1;
-      load(q + GP_CW * 32, n0, n1);
+      load(q + GP_CW * 32, nxt, n0, n1);
 #else
       NodeD c0d, c1d;
-      load(q, c0d, c1d);
+      load(q, cur, c0d, c1d);
 #endif
+      const Pos at = cur;
+      cur = nxt;
+      advance(nxt);
       if (q < total) {
-        int r, ry2, g;
-        decode(q, r, ry2, g);
+        const int r = at.r, ry2 = at.ry, g = at.g;
         const int i = x0 + r, j = y0 + GP_ROWS * ry2;
         if (j < Ny) {
           const float* pl[5];
+          const float* p0 = sm + GP_ROWS * ry2 * P;
 #pragma unroll
-          for (int a = 0; a < 5; ++a)
-            pl[a] = sm + (size_t)((base + r + a) % GP_RING) * slot_floats + GP_ROWS * ry2 * P;
+          for (int a = 0; a < 5; ++a) {
+            const int sl = at.slot + a;
+            pl[a] = p0 + (sl >= GP_RING ? sl - GP_RING : sl) * slot_floats;
+          }
           const int offA = g == 0 ? Nz - 4 : 4 * g - 4, offB = 4 * g;
           if (GP_ROWS == 2)
             gp_item<FG, P>(c0d, c1d, pl, R * P, offA, offB, coef, disp, out, N, c0, i, j, g, Nx, Ny, Nz, sc);
           else
-            gp_item1<FG, P>(c0d, pl, R * P, offA, offB, coef, disp, out, N, c0, i, j, g, Nx, Ny, Nz, sc);
+            gp_item1<FG, P, UNIT>(c0d, pl, R * P, offA, offB, coef, disp, out, N, c0, i, j, g, Nx, Ny, Nz, sc);
         }
       }
     }
@@ -487,16 +517,21 @@ void gp_launch(const float* coef, int ncomp, const float* disp, float* out, cons
   gp_encode(&tb, coef, ncomp, N, P, std::min(R, N[1]));
   gp_encode(&tr, coef, ncomp, N, P, 2);
   const size_t smem = (size_t)GP_RING * FG * R * P * sizeof(float);
-  static bool attr_set[64] = {};
-  int dev = 0;
-  LDDMM_CUDA(cudaGetDevice(&dev));
-  if (!attr_set[dev & 63]) {
-    LDDMM_CUDA(cudaFuncSetAttribute(gather_pipe_kernel<FG, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)GP_SMEM_MAX));
-    attr_set[dev & 63] = true;
-  }
-  pdl_launch(gather_pipe_kernel<FG, P>, dim3(nseg, tiles_y, 1), GP_NTH, smem, s, tb, tr, coef, ncomp, disp, out, N[0], N[1],
-                                                                       N[2], sc, TY, seg);
+  auto go = [&](auto kern, int slot) {
+    static bool attr_set[64][2] = {};
+    int dev = 0;
+    LDDMM_CUDA(cudaGetDevice(&dev));
+    if (!attr_set[dev & 63][slot]) {
+      LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM_MAX));
+      attr_set[dev & 63][slot] = true;
+    }
+    pdl_launch(kern, dim3(nseg, tiles_y, 1), GP_NTH, smem, s, tb, tr, coef, ncomp, disp, out, N[0], N[1], N[2], sc,
+               TY, seg);
+  };
+  if (sc.x == 1.f && sc.y == 1.f && sc.z == 1.f)
+    go(gather_pipe_kernel<FG, P, true>, 0);
+  else
+    go(gather_pipe_kernel<FG, P, false>, 1);
   LDDMM_LAUNCH_CHECK();
 }
 
