@@ -58,7 +58,10 @@ namespace {
 #ifndef GP_PREFETCH
 #define GP_PREFETCH 1
 #endif
-constexpr int GP_RING = 6;
+#ifndef GP_RING_N
+#define GP_RING_N 6
+#endif
+constexpr int GP_RING = GP_RING_N;  // staged planes (lab: -DGP_RING_N=7 with TY = 10)
 #ifndef GP_THREADS
 #define GP_THREADS 384
 #endif
