@@ -207,6 +207,32 @@ void launch_nonfinite_flag(long long n, const double2* x, double* part, double* 
   LDDMM_LAUNCH_CHECK();
 }
 
+// Non-finite flags of `count` consecutive series nodes (node j = base + j V) in one
+// launch: a thread that meets a non-finite value stores 1 into its node's step slot
+// (every writer stores the same value); the slots are zeroed by the caller beforehand.
+// Step of node j: step0 + j, or step0 + count - 1 - j for a backward march.
+__global__ __launch_bounds__(256) void nonfinite_series_kernel(const double2* __restrict__ base, long long V,
+                                                               int count, int step0, int backward,
+                                                               double* __restrict__ slots) {
+  pdl_prologue();
+  const long long n = V * count;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = base[i];
+    if (!isfinite(a.x) || !isfinite(a.y)) {
+      const int j = (int)(i / V);
+      slots[backward ? step0 + count - 1 - j : step0 + j] = 1.0;
+    }
+  }
+}
+
+void launch_nonfinite_series(const double2* base, long long V, int count, int step0, bool backward, double* slots,
+                             cudaStream_t s) {
+  LDDMM_CUDA(cudaMemsetAsync(slots + step0, 0, count * sizeof(double), s));
+  pdl_launch(nonfinite_series_kernel, grid_for(V * count, 256), 256, 0, s, base, V, count, step0, backward ? 1 : 0,
+             slots);
+  LDDMM_LAUNCH_CHECK();
+}
+
 int launch_nonfinite_partial(long long n, const double2* x, double* part, cudaStream_t s) {
   const int g = red_grid(n);
   pdl_launch(nonfinite_partial_kernel, g, 256, 0, s, n, x, part);

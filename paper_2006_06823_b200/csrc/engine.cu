@@ -653,9 +653,11 @@ void Engine::finish_finite_checks(int nsteps) {
 void Engine::check_series_finite(const double2* series, int count, int first, bool backward) {
   const long long V = vec_elems();
   const int nt = prob_.nt;
-  for (int s = first; s < first + count; ++s) {
-    const int to = backward ? nt - s - 1 : s + 1;
-    enqueue_finite_check(series + to * V, s);
+  if (count > 0) {
+    // steps first .. first + count - 1 fill nodes first + 1 .. (forward) or nt - first - 1
+    // down to nt - first - count (backward): one contiguous range, one launch
+    const int lo = backward ? nt - first - count : first + 1;
+    launch_nonfinite_series(series + lo * V, V, count, first, backward, slots_.p + 16, stream_);
   }
   finish_finite_checks(first + count);
 }

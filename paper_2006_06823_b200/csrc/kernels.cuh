@@ -162,6 +162,10 @@ int launch_nonfinite_partial(long long n, const double2* x, double* part, cudaSt
 // 1.0 into *slot when x holds a non-finite value, else 0.0; part needs kReduceBlocks + 1
 // doubles, the last one a zero-initialised counter
 void launch_nonfinite_flag(long long n, const double2* x, double* part, double* slot, cudaStream_t s);
+// flags of `count` consecutive nodes base + j V into slots[step], step = step0 + j (or
+// step0 + count - 1 - j backward), one launch (the slots are zeroed first)
+void launch_nonfinite_series(const double2* base, long long V, int count, int step0, bool backward, double* slots,
+                             cudaStream_t s);
 void launch_reduce_final(const double* part, int nparts, int op /*0 sum 1 max*/, double* slot, cudaStream_t s);
 
 // ---- grid pointwise (fp32 fields, fp64 reductions) --------------------------------
