@@ -213,14 +213,14 @@ def run_reference(args, rank, world):
 
 
 def ncu_traffic():
-    """DRAM bytes of one captured gather launch (profiles/r1_ncu_traffic.json, from
+    """DRAM bytes of one captured gather launch (profiles/r2s2_ncu_traffic.json, from
     `ncu --set full`), next to that launch's algorithmic bytes N (12 + 8 F)."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r2s2_ncu_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
         return {"traffic": t["dram_bytes"], "traffic_launch_algorithmic_bytes": t["algorithmic_bytes"],
-                "traffic_source": "profiles/r1_ncu_traffic.json (" + t["kernel"] + ", one launch)"}
+                "traffic_source": "profiles/r2s2_ncu_traffic.json (" + t["kernel"] + ", one launch)"}
     except (OSError, KeyError, ValueError):
         return {"traffic": None}
 
