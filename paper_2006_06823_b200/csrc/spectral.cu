@@ -215,15 +215,18 @@ __global__ __launch_bounds__(256) void cgemm_kernel(const float2* __restrict__ A
 
 // ---------------------------------------------------------------------------
 // batched real GEMM for the Z stages: C[b][m][n] = sum_k A[b][m][k] * B[k][n]
-// BM = 128, BK = 16, thread tile 8 x 4.  BN = 64 (256 threads) or 32 (128 threads).
+// BM = 128 (or 32 for grids with few row tiles: 4x the CTAs), BK = 16, thread tile RT x 4
+// (RT = 8 or 2).  BN = 64 (256 threads) or 32 (128 threads).  Every output sums its K terms
+// in the same order for any BM.
 
-template <int BN>
+template <int BN, int BM = 128>
 __global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__ A, int lda, long long sA,
                                                        const float* __restrict__ B, int ldb,
                                                        float* __restrict__ C, int ldc, long long sC, int M,
                                                        int N, int K) {
   pdl_prologue();
-  constexpr int BM = 128, BK = 16, NT = BN * 4, TXN = BN / 4;
+  constexpr int BK = 16, NT = BN * 4, TXN = BN / 4, RT = BM * TXN / NT;
+  static_assert(RT == 8 || RT == 2, "thread tile rows");
   __shared__ __align__(16) float As[BK][BM + 4];
   __shared__ __align__(16) float Bs[BK][BN];
   const int tid = threadIdx.x;
@@ -231,9 +234,9 @@ __global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   A += blockIdx.z * sA;
   C += blockIdx.z * sC;
-  float acc[8][4];
+  float acc[RT][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < RT; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   for (int k0 = 0; k0 < K; k0 += BK) {
@@ -252,13 +255,20 @@ __global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+      float av[RT];
+      if constexpr (RT == 8) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+        av[0] = a0.x, av[1] = a0.y, av[2] = a0.z, av[3] = a0.w, av[4] = a1.x, av[5] = a1.y, av[6] = a1.z,
+        av[7] = a1.w;
+      } else {
+        const float2 a0 = *reinterpret_cast<const float2*>(&As[kk][ty * 2]);
+        av[0] = a0.x, av[1] = a0.y;
+      }
       const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
@@ -266,8 +276,8 @@ __global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__
   }
   const int gn = n0 + tx * 4;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int gm = m0 + ty * 8 + i;
+  for (int i = 0; i < RT; ++i) {
+    const int gm = m0 + ty * RT + i;
     if (gm >= M) break;
     float* crow = C + (long long)gm * ldc;
     if (gn + 3 < N && (ldc & 3) == 0) {
@@ -518,7 +528,11 @@ void launch_cgemm(const float2* A, int lda, const float2* B, long long sB, int l
 
 void launch_sgemm(const float* A, int lda, long long sA, const float* B, int ldb, float* C, int ldc,
                   long long sC, int M, int N, int K, int batch, cudaStream_t s) {
-  if (N <= 32) {
+  if (N <= 32 && (long long)ceil_div(M, 128) * batch < kSMs) {
+    // few row tiles (the small product grid's z-project: 51 CTAs): 32-row tiles
+    dim3 grid(ceil_div(N, 32), ceil_div(M, 32), batch);
+    pdl_launch(sgemm_kernel<32, 32>, grid, 128, 0, s, A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
+  } else if (N <= 32) {
     dim3 grid(ceil_div(N, 32), ceil_div(M, 128), batch);
     pdl_launch(sgemm_kernel<32>, grid, 128, 0, s, A, lda, sA, B, ldb, C, ldc, sC, M, N, K);
   } else {
