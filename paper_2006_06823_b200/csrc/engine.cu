@@ -219,10 +219,12 @@ void Engine::build_plan(DftPlan& p, const int* Ng, const int* K, const double* w
     p.uz_p_small = alloc(nc);
     launch_umma_zproj_prep(p.tz_p_big, p.tz_p_small, Nz, 2 * H, p.uz_p_big, p.uz_p_small, stream_);
   }
-  // x stage on tcgen05 (twiddles as the canonical K-major operand) where the plan fits, on
-  // the full grid (the small product grid's transforms are launch-latency-bound: FFMA)
-  const bool small_grid = Ntot < (double)(1 << 20) && !std::getenv("LDDMM_UMMA_X_SMALL");
-  if (!small_grid && !(std::getenv("LDDMM_UMMA_X") && std::getenv("LDDMM_UMMA_X")[0] == '0')) {
+  // x stage on tcgen05 (twiddles as the canonical K-major operand) where the plan fits and
+  // a field has enough 128-column tiles (2 Ny H >= 4096: config 2's full grid, config 4's
+  // 94^3 product grid); narrower transforms (config 2's 46^3 product grid) are
+  // launch-latency-bound and stay on FFMA
+  const bool narrow = 2LL * Ny * H < 4096 && !std::getenv("LDDMM_UMMA_X_SMALL");
+  if (!narrow && !(std::getenv("LDDMM_UMMA_X") && std::getenv("LDDMM_UMMA_X")[0] == '0')) {
     std::vector<float> tw;
     if (umma_xstage_fits(Nx, Kx, Ny * H)) {
       umma_xstage_twiddles_host(wx_e.data(), Nx, Kx, tw);
