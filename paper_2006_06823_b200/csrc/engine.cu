@@ -207,6 +207,13 @@ void Engine::build_plan(DftPlan& p, const int* Ng, const int* K, const double* w
     plan_allocs_.push_back(d);
     return (float*)d;
   };
+  {
+    void* d = nullptr;
+    LDDMM_CUDA(cudaMalloc(&d, (size_t)(Kx + Ky + K[2]) * sizeof(double)));
+    plan_allocs_.push_back(d);
+    p.bsym = (double*)d;
+    launch_band_symbols(K, Ng, p.bsym, stream_);
+  }
   p.tz_e_big = alloc(tz_e.size());
   p.tz_e_small = alloc(tz_e.size());
   p.tz_p_big = alloc(tz_p.size());

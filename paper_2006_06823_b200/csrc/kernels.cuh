@@ -63,12 +63,15 @@ struct DftPlan {
   // Wx_e / Wx_p as the tcgen05 x-stage twiddle operand (umma_xstage.cu: real / imaginary x
   // TF32 big / small, canonical K-major), or null (FFMA x stage)
   float *ux_e = nullptr, *ux_p = nullptr;
+  // B(k) factors of the prefilter symbol per axis [Kx | Ky | Kz] (launch_band_symbols)
+  double* bsym = nullptr;
   long long npts() const { return (long long)N[0] * N[1] * N[2]; }
   long long half() const { return (long long)K[0] * K[1] * (K[2] / 2); }
   long long kprod() const { return (long long)K[0] * K[1] * K[2]; }
 };
 
 void launch_band_prep(const PrepArgs& a, const DftPlan& p, float2* D, cudaStream_t s);
+void launch_band_symbols(const int* K, const int* N, double* out, cudaStream_t s);
 void launch_band_finalize(const FinArgs& a, const DftPlan& p, const float2* G, cudaStream_t s);
 void dft_embed_prep(const DftPlan& p, const PrepArgs& a, float2* D, float2* E1, float2* E2, float* out,
                     cudaStream_t s);

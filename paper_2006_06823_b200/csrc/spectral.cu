@@ -32,7 +32,8 @@ namespace lddmm_b200 {
 
 // element (f, fx, fy, fz) of the fp32 half band D (fold, symbols, scale)
 __device__ __forceinline__ float2 prep_value(const PrepArgs& a, int f, int fx, int fy, int fz, int Kx, int Ky, int Kz,
-                                             int Nx, int Ny, int Nz, double wx, double wy, double wz) {
+                                             int Nx, int Ny, int Nz, double wx, double wy, double wz,
+                                             const double* __restrict__ bsym) {
   float2 out = make_float2(0.f, 0.f);
   const PrepField pf = a.f[f];
   if (fx != Kx / 2 && fy != Ky / 2 && pf.src != nullptr) {
@@ -51,9 +52,9 @@ __device__ __forceinline__ float2 prep_value(const PrepArgs& a, int f, int fx, i
     if (pf.sym & SYM_PREFILTER) {
       // 1 / B(k), B(k) = prod_a (4 + 2 cos(2 pi k_a / N_a)) / 6 (exact periodic cubic
       // B-spline prefilter of interp.hpp:23-63 in Fourier form)
-      const double bx = (4.0 + 2.0 * cospi(2.0 * kx / Nx)) / 6.0;
-      const double by = (4.0 + 2.0 * cospi(2.0 * ky / Ny)) / 6.0;
-      const double bz = (4.0 + 2.0 * cospi(2.0 * kz / Nz)) / 6.0;
+      // per-axis factors from the plan's table (band_symbol_kernel: the same expressions,
+      // so the same doubles as evaluating them here)
+      const double bx = __ldg(bsym + fx), by = __ldg(bsym + Kx + fy), bz = __ldg(bsym + Kx + Ky + fz);
       s /= (bx * by * bz);
     }
     const int dax = pf.sym & SYM_DERIV_MASK;
@@ -69,8 +70,33 @@ __device__ __forceinline__ float2 prep_value(const PrepArgs& a, int f, int fx, i
   return out;
 }
 
+// B(k) factors (4 + 2 cos(2 pi k_a / N_a)) / 6 per axis and band index (signed frequency),
+// concatenated [Kx | Ky | Kz], for the prefilter symbol of prep_value
+__global__ void band_symbol_kernel(int Kx, int Ky, int Kz, int Nx, int Ny, int Nz, double* __restrict__ out) {
+  pdl_prologue();
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Kx + Ky + Kz; t += gridDim.x * blockDim.x) {
+    double v;
+    if (t < Kx) {
+      const int kx = t < Kx / 2 ? t : t - Kx;
+      v = (4.0 + 2.0 * cospi(2.0 * kx / Nx)) / 6.0;
+    } else if (t < Kx + Ky) {
+      const int f = t - Kx, ky = f < Ky / 2 ? f : f - Ky;
+      v = (4.0 + 2.0 * cospi(2.0 * ky / Ny)) / 6.0;
+    } else {
+      const int kz = t - Kx - Ky;
+      v = (4.0 + 2.0 * cospi(2.0 * kz / Nz)) / 6.0;
+    }
+    out[t] = v;
+  }
+}
+
+void launch_band_symbols(const int* K, const int* N, double* out, cudaStream_t s) {
+  pdl_launch(band_symbol_kernel, 1, 256, 0, s, K[0], K[1], K[2], N[0], N[1], N[2], out);
+  LDDMM_LAUNCH_CHECK();
+}
+
 __global__ void band_prep_kernel(PrepArgs a, int Kx, int Ky, int Kz, int Nx, int Ny, int Nz, double wx,
-                                 double wy, double wz, float2* __restrict__ D) {
+                                 double wy, double wz, const double* __restrict__ bsym, float2* __restrict__ D) {
   pdl_prologue();
   const int H = Kz / 2;
   const long long per = (long long)Kx * Ky * H;
@@ -83,7 +109,7 @@ __global__ void band_prep_kernel(PrepArgs a, int Kx, int Ky, int Kz, int Nx, int
     r /= H;
     const int fy = (int)(r % Ky);
     const int fx = (int)(r / Ky);
-    D[t] = prep_value(a, f, fx, fy, fz, Kx, Ky, Kz, Nx, Ny, Nz, wx, wy, wz);
+    D[t] = prep_value(a, f, fx, fy, fz, Kx, Ky, Kz, Nx, Ny, Nz, wx, wy, wz, bsym);
   }
 }
 
@@ -296,7 +322,7 @@ __global__ __launch_bounds__(BN * 4) void sgemm_kernel(const float* __restrict__
 void launch_band_prep(const PrepArgs& a, const DftPlan& p, float2* D, cudaStream_t s) {
   const long long total = (long long)p.K[0] * p.K[1] * (p.K[2] / 2) * a.nf;
   pdl_launch(band_prep_kernel, grid_for(total, 256), 256, 0, s, a, p.K[0], p.K[1], p.K[2], p.N[0], p.N[1], p.N[2],
-                                                        p.omega_unit[0], p.omega_unit[1], p.omega_unit[2], D);
+                                                        p.omega_unit[0], p.omega_unit[1], p.omega_unit[2], p.bsym, D);
   LDDMM_LAUNCH_CHECK();
 }
 
@@ -316,6 +342,7 @@ struct PrepCtx {
   PrepArgs a;
   int Kx, Ky, Kz, Nx, Ny, Nz;
   double wx, wy, wz;
+  const double* bsym;  // the plan's B(k) factor table (band_symbol_kernel)
 };
 
 struct FinCtx {
@@ -364,7 +391,13 @@ struct CgemmSplit {
 
 static CgemmSplit cgemm_split(int M, int N, int K, int batch) {
   CgemmSplit sp;
-  sp.MS = batch < 2 * kSMs && M >= 8 ? 2 : 1;
+  // 2 (or 4) CTAs per batch item when the grid is short of CTAs or one CTA's twiddle slab
+  // (M (K + 1) complex) would hold an SM alone (config 4: 131 KB -> 1 CTA of 8 warps per SM)
+  const size_t slab = (size_t)M * (K + 1) * sizeof(float2);
+  const int msplit = std::getenv("LDDMM_Y_MS") ? std::atoi(std::getenv("LDDMM_Y_MS")) : 0;  // lab override
+  sp.MS = M >= 8 && (batch < 2 * kSMs || slab > 64 * 1024) ? 2 : 1;
+  if (M >= 16 && slab > 128 * 1024) sp.MS = 4;
+  if (msplit > 0) sp.MS = msplit;
   sp.mrows = ((M + sp.MS - 1) / sp.MS + 1) & ~1;
   const int tiles = (sp.mrows / 2) * ((N + 1) / 2);
   sp.KS = 1;
@@ -403,7 +436,7 @@ __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restric
     const int f = b / pc.Kx, fx = b - f * pc.Kx;
     for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
       const int k = e / N, n = e - (e / N) * N;
-      Bs[e] = prep_value(pc.a, f, fx, k, n, pc.Kx, pc.Ky, pc.Kz, pc.Nx, pc.Ny, pc.Nz, pc.wx, pc.wy, pc.wz);
+      Bs[e] = prep_value(pc.a, f, fx, k, n, pc.Kx, pc.Ky, pc.Kz, pc.Nx, pc.Ny, pc.Nz, pc.wx, pc.wy, pc.wz, pc.bsym);
     }
   } else {
     const float2* Bb = B + b * sB;
@@ -588,6 +621,7 @@ void dft_embed_prep(const DftPlan& p, const PrepArgs& a, float2* D, float2* E1, 
   pc.a = a;
   pc.Kx = Kx, pc.Ky = Ky, pc.Kz = p.K[2], pc.Nx = p.N[0], pc.Ny = p.N[1], pc.Nz = p.N[2];
   pc.wx = p.omega_unit[0], pc.wy = p.omega_unit[1], pc.wz = p.omega_unit[2];
+  pc.bsym = p.bsym;
   static const FinCtx nofin{};
   launch_cgemm_smem<1>(p.wy_e, Ky, nullptr, 0, H, E1, (long long)Ny * H, H, Ny, H, Ky, a.nf * Kx, pc, nofin, s);
   dft_embed_xz(p, a.nf, E1, E2, out, s);
