@@ -383,6 +383,13 @@ def main():
     value = total_ms / 1000.0 / (world * args.steps)
     hbm, peak_kind = peaks()
     achieved = (g_bytes / g_n) / (g_ms / g_n * 1e-3) / 1e9 if g_n else 0.0
+    # the same gathers against the FP32 pipe: component-samples sum C N over the launches
+    # (bytes = N (12 + 8 C) per launch), 84 FMA per sample for the exact separable 4-tap
+    # stencil (64 z-dots + 16 + 4) and 150 for the 5 x 5-row / 5-tap window form the
+    # kernel executes (DESIGN 4.1); 2 flop per FMA
+    npts = float(np.prod(DIMS))
+    g_samples = (g_bytes - 12.0 * npts * g_n) / 8.0 if g_n else 0.0
+    g_s = g_ms * 1e-3 if g_n else 1.0
     fp32, fp32_kind = fp32_peak()
     dft_tflops = d_flops / (d_ms * 1e-3) / 1e12 if d_n else 0.0
 
@@ -462,7 +469,15 @@ def main():
                             "frac": achieved / hbm, **ncu_traffic(),
                             "algorithmic_bytes_per_launch": g_bytes / g_n if g_n else 0,
                             "launches_timed": g_n, "gather_share_of_step": g_ms / total_ms if total_ms else 0},
-               "roofline_dft": {"kernel": "full-grid truncated DFT pipelines (y/x FFMA GEMMs + tcgen05 z stage)",
+               "roofline_gather_fp32": {"kernel": "gather_pipe_kernel", "bound": "fp32", "unit": "TFLOP/s",
+                                        "achieved_minimal": 2 * 84 * g_samples / g_s / 1e12,
+                                        "achieved_executed": 2 * 150 * g_samples / g_s / 1e12,
+                                        "peak": fp32, "peak_kind": fp32_kind,
+                                        "frac_minimal": 2 * 84 * g_samples / g_s / 1e12 / fp32,
+                                        "frac_executed": 2 * 150 * g_samples / g_s / 1e12 / fp32,
+                                        "fma_per_sample": {"minimal": 84, "executed": 150},
+                                        "component_samples": g_samples},
+               "roofline_dft": {"kernel": "full-grid truncated DFT pipelines (y FFMA GEMMs + tcgen05 x / z stages)",
                                 "bound": "fp32", "achieved": dft_tflops, "peak": fp32, "peak_kind": fp32_kind,
                                 "unit": "TFLOP/s", "frac": dft_tflops / fp32, "traffic": None,
                                 "flops_per_field": dft_flops_per_field(),
