@@ -468,6 +468,36 @@ __global__ __launch_bounds__(256) void cgemm_smem_kernel(const float2* __restric
     }
   };
   const int kslice = (K + KS - 1) / KS;
+  // tall shapes (the y-embed: M = Ny rows): 4 x 2 output tiles per thread, the two B
+  // values of a k step shared by four rows (6 shared loads per 32 FMA instead of 4 per 16);
+  // every output still sums its K terms in order
+  const int tiles4 = ((mh + 3) / 4) * tn;
+  if (KS == 1 && tiles4 >= 128) {
+    for (int t = threadIdx.x; t < tiles4; t += blockDim.x) {
+      const int m0 = (t / tn) * 4, n0 = (t - (t / tn) * tn) * 2;
+      const int n1 = min(n0 + 1, N - 1);
+      const float2* ap[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ap[i] = As + min(m0 + i, mh - 1) * KP;
+      float2 c[4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) {
+        const float2 b0 = Bs[k * N + n0], b1 = Bs[k * N + n1];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 a = ap[i][k];
+          c[i][0].x = fmaf(a.x, b0.x, fmaf(-a.y, b0.y, c[i][0].x));
+          c[i][0].y = fmaf(a.x, b0.y, fmaf(a.y, b0.x, c[i][0].y));
+          c[i][1].x = fmaf(a.x, b1.x, fmaf(-a.y, b1.y, c[i][1].x));
+          c[i][1].y = fmaf(a.x, b1.y, fmaf(a.y, b1.x, c[i][1].y));
+        }
+      }
+      emit(m0, n0, c[0][0], c[0][1], c[1][0], c[1][1]);
+      if (m0 + 2 < mh) emit(m0 + 2, n0, c[2][0], c[2][1], c[3][0], c[3][1]);
+    }
+  } else
   for (int it = threadIdx.x; it < tiles * KS; it += blockDim.x) {
     const int t = it % tiles, ks = it / tiles;
     const int m0 = (t / tn) * 2, n0 = (t - (t / tn) * tn) * 2;
