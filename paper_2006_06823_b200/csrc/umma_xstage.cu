@@ -101,12 +101,13 @@ __device__ __forceinline__ void xs_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // tmX: X as float [nf][K][N2] (box {32, XS_KC, 1}, SWIZZLE_128B); Tw: 4 canonical
 // K-major arrays [Mpad][Kpad] (W real big, real small, imag big, imag small); C[f][m][n']
 // with row pitch N2 and field stride sC.  NG: MMA N (output rows m per group), G groups.
-template <int TMEM_COLS>
+template <int TMEM_COLS, int NBUF, int NSB>
 __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid_constant__ CUtensorMap tmX,
                                                                     const float* __restrict__ Tw,
                                                                     float* __restrict__ C, long long sC, int M,
                                                                     int N2, int Kpad, int Mpad, int nf, int NG,
-                                                                    int G, int NACC, int UC) {
+                                                                    int G, int NACC, int UC, int gsplit,
+                                                                    int single) {
   constexpr uint32_t LBO_B = 128;
   const uint32_t SBO_B = (uint32_t)(Kpad / 4) * 128;
   // TMEM: NACC buffers of UC columns per accumulator unit: with several k chunks one (P, Q)
@@ -116,9 +117,9 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
   // tolerance; 32 terms deep it does not.
   extern __shared__ __align__(1024) float sm[];
   float* ring = sm;                        // NBUF raw chunks (TMA destination, [4 boxes][KC][32])
-  float* opb = ring + XS_NBUF * XS_CH;     // NSB x (big, small) canonical K-major chunks
-  float* tw = opb + 2 * XS_NSB * XS_CH;    // 4 x Mpad x Kpad
-  __shared__ __align__(8) unsigned long long full[XS_NBUF], consumed[XS_NBUF], ready[XS_NSB], mma_done[XS_NSB];
+  float* opb = ring + NBUF * XS_CH;     // NSB x (big, small) canonical K-major chunks
+  float* tw = opb + 2 * NSB * XS_CH;    // 4 x Mpad x Kpad
+  __shared__ __align__(8) unsigned long long full[NBUF], consumed[NBUF], ready[NSB], mma_done[NSB];
   __shared__ __align__(8) unsigned long long acc_full[2], acc_free[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -126,7 +127,7 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
   // split by warps 2-3; several chunks (project: K = Nx) -> the split dominates: 4
   // epilogue warps (4-7), split by warps 2-3 and 8-15
   const int nk = Kpad / XS_KC;
-  const int EW = nk == 1 ? 3 : 1;                 // epilogue warps per TMEM lane quarter
+  const int EW = (nk == 1 || single) ? 3 : 1;     // epilogue warps per TMEM lane quarter
   const int NSPLIT = (XS_THREADS / 32 - 4 - 4 * EW + 2) * 32;  // split threads
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(xs_su32(&tmem_base_sh)),
@@ -134,11 +135,11 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    for (int i = 0; i < XS_NBUF; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xs_su32(&full[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(xs_su32(&consumed[i])), "r"(NSPLIT));
     }
-    for (int i = 0; i < XS_NSB; ++i) {
+    for (int i = 0; i < NSB; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(xs_su32(&ready[i])), "r"(NSPLIT));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xs_su32(&mma_done[i])));
     }
@@ -148,8 +149,15 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int e = tid; e < Mpad * Kpad; e += XS_THREADS)  // 4 arrays, float4 each
-    reinterpret_cast<float4*>(tw)[e] = __ldg(reinterpret_cast<const float4*>(Tw) + e);
+  // gsplit: CTA b handles output-row group g0 = b % G of its tiles only and keeps that
+  // group's twiddle rows (4 NG canonical rows, contiguous); otherwise all groups
+  const int g0 = gsplit ? (int)blockIdx.x % G : 0, Gc = gsplit ? 1 : G;
+  const int cta = gsplit ? (int)blockIdx.x / G : (int)blockIdx.x, nct = gsplit ? (int)gridDim.x / G : (int)gridDim.x;
+  {
+    const float4* src = reinterpret_cast<const float4*>(Tw) + (size_t)g0 * NG * Kpad;  // 4 NG Kpad floats per group
+    const int n4 = (gsplit ? NG : Mpad) * Kpad;
+    for (int e = tid; e < n4; e += XS_THREADS) reinterpret_cast<float4*>(tw)[e] = __ldg(src + e);
+  }
   // TMEM, barriers and the (constant) twiddle operand are set up before the PDL wait
   pdl_wait();
   pdl_trigger();
@@ -160,7 +168,8 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
   const uint32_t tmem = tmem_base_sh;
   const int ntn = (N2 + 127) / 128;  // 128-column tiles per field
   const int T = nf * ntn;
-  const int my_tiles = (T - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int my_tiles = (T - cta + nct - 1) / nct;
+  const bool sep = nk > 1 && !single;  // per-chunk accumulators + corrections
   const int S = my_tiles * nk;  // this CTA's chunk sequence
   auto par = [](int q, int period) { return (uint32_t)(q / period) & 1u; };
 
@@ -168,14 +177,14 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
     if (lane == 0) {
       // TMA producer: chunk q -> ring slot q % NBUF once chunk q - NBUF has been transposed
       for (int q = 0; q < S; ++q) {
-        if (q >= XS_NBUF) xs_wait(&consumed[q % XS_NBUF], par(q - XS_NBUF, XS_NBUF));
-        const int tile = (int)blockIdx.x + (q / nk) * (int)gridDim.x, j = q % nk;
+        if (q >= NBUF) xs_wait(&consumed[q % NBUF], par(q - NBUF, NBUF));
+        const int tile = cta + (q / nk) * nct, j = q % nk;
         const int f = tile / ntn, n0 = (tile - f * ntn) * 128;
-        unsigned long long* bar = &full[q % XS_NBUF];
+        unsigned long long* bar = &full[q % NBUF];
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xs_su32(bar)),
                      "r"((uint32_t)(XS_CH * 4))
                      : "memory");
-        float* dst = ring + (q % XS_NBUF) * XS_CH;
+        float* dst = ring + (q % NBUF) * XS_CH;
         for (int b = 0; b < 4; ++b)
           asm volatile(
               "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -195,15 +204,15 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
       const uint32_t tw0 = xs_su32(tw);
       for (int s = 0; s < S; ++s) {
         const int t = s / nk, j = s % nk;
-        xs_wait(&ready[s % XS_NSB], par(s, XS_NSB));
+        xs_wait(&ready[s % NSB], par(s, NSB));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t a_big = xs_su32(opb + (s % XS_NSB) * 2 * XS_CH), a_sml = a_big + XS_CH * 4;
-        for (int g = 0; g < G; ++g) {
-          const int u = t * G + g;  // accumulator unit
+        const uint32_t a_big = xs_su32(opb + (s % NSB) * 2 * XS_CH), a_sml = a_big + XS_CH * 4;
+        for (int g = 0; g < Gc; ++g) {
+          const int u = t * Gc + g;  // accumulator unit
           if (j == 0 && u >= NACC) xs_wait(&acc_free[u % NACC], par(u - NACC, NACC));
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t ub = tmem + (uint32_t)((u % NACC) * UC);
-          const uint32_t big = ub + (uint32_t)(j * 2 * NG), corr = nk > 1 ? ub + (uint32_t)(nk * 2 * NG) : big;
+          const uint32_t big = sep ? ub + (uint32_t)(j * 2 * NG) : ub, corr = sep ? ub + (uint32_t)(nk * 2 * NG) : big;
           // twiddle rows g 4 NG .. (8-row groups SBO_B apart), k chunk j (XS_KC / 4 core matrices of 128 B)
           const uint32_t wb = tw0 + (uint32_t)(g * 4 * NG / 8) * SBO_B + (uint32_t)j * (XS_KC / 4) * 128;
           const uint32_t ws = wb + (uint32_t)(2 * NG / 8) * SBO_B;
@@ -211,8 +220,8 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
             const uint64_t adb = xs_desc_k(a_big + ks * 2 * LBO_B, LBO_B, SBO_A);
             const uint64_t ads = xs_desc_k(a_sml + ks * 2 * LBO_B, LBO_B, SBO_A);
             const uint64_t bdb = xs_desc_k(wb + ks * 2 * LBO_B, LBO_B, SBO_B);
-            xs_mma(big, adb, bdb, idesc2, ks ? 1u : 0u);
-            xs_mma(corr, adb, xs_desc_k(ws + ks * 2 * LBO_B, LBO_B, SBO_B), idesc2, (nk == 1 || j | ks) ? 1u : 0u);
+            xs_mma(big, adb, bdb, idesc2, (sep ? ks : (j | ks)) ? 1u : 0u);
+            xs_mma(corr, adb, xs_desc_k(ws + ks * 2 * LBO_B, LBO_B, SBO_B), idesc2, (!sep || j | ks) ? 1u : 0u);
             xs_mma(big, ads, bdb, idesc2, 1u);
           }
           if (j == nk - 1)
@@ -221,7 +230,7 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
                          : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         xs_su32(&mma_done[s % XS_NSB]))
+                         xs_su32(&mma_done[s % NSB]))
                      : "memory");
       }
     }
@@ -231,12 +240,12 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
     const int qd = warp & 3, part = (warp - 4) >> 2;
     const bool odd = lane & 1;
     for (int t = 0; t < my_tiles; ++t) {
-      const int tile = (int)blockIdx.x + t * (int)gridDim.x;
+      const int tile = cta + t * nct;
       const int f = tile / ntn, n = (tile - f * ntn) * 128 + qd * 32 + lane;
       const bool nok = n < N2;
       float* cf = C + (long long)f * sC + n;
-      for (int g = 0; g < G; ++g) {
-        const int u = t * G + g;
+      for (int g = 0; g < Gc; ++g) {
+        const int u = t * Gc + g;
         xs_wait(&acc_full[u % NACC], par(u, NACC));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t ub = tmem + (uint32_t)((u % NACC) * UC) + ((uint32_t)(qd * 32) << 16);
@@ -245,14 +254,14 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
           {
             // corrections (several chunks) or the single chunk's accumulator
             uint32_t p[16], q[16];
-            const uint32_t c = nk > 1 ? (uint32_t)(nk * 2 * NG) : 0u;
+            const uint32_t c = sep ? (uint32_t)(nk * 2 * NG) : 0u;
             xs_ld16(ub + c + c0, p);
             xs_ld16(ub + c + (uint32_t)NG + c0, q);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 16; ++i) ps[i] = __uint_as_float(p[i]), qs[i] = __uint_as_float(q[i]);
           }
-          for (int j = 0; j < (nk > 1 ? nk : 0); ++j) {  // k chunks summed in fp32
+          for (int j = 0; j < (sep ? nk : 0); ++j) {  // k chunks summed in fp32
             uint32_t p[16], q[16];
             xs_ld16(ub + (uint32_t)(j * 2 * NG) + c0, p);
             xs_ld16(ub + (uint32_t)(j * 2 * NG + NG) + c0, q);
@@ -266,7 +275,7 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
             const float qo = __shfl_xor_sync(0xffffffffu, qs[i], 1);
             v[i] = odd ? ps[i] + qo : ps[i] - qo;
           }
-          const int m0 = g * NG + c0;
+          const int m0 = (g0 + g) * NG + c0;
           float* cp = cf + (long long)m0 * N2;
           if (nok && m0 + 16 <= M) {
 #pragma unroll
@@ -289,10 +298,10 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
     // core-matrix row.
     const int st = warp < 4 ? tid - 64 : tid - 64 - 128 * EW;
     for (int s = 0; s < S; ++s) {
-      xs_wait(&full[s % XS_NBUF], par(s, XS_NBUF));
-      if (s >= XS_NSB) xs_wait(&mma_done[s % XS_NSB], par(s - XS_NSB, XS_NSB));
-      const float* raw = ring + (s % XS_NBUF) * XS_CH;
-      float* big = opb + (s % XS_NSB) * 2 * XS_CH;
+      xs_wait(&full[s % NBUF], par(s, NBUF));
+      if (s >= NSB) xs_wait(&mma_done[s % NSB], par(s - NSB, NSB));
+      const float* raw = ring + (s % NBUF) * XS_CH;
+      float* big = opb + (s % NSB) * 2 * XS_CH;
       float* sml = big + XS_CH;
       for (int item = st; item < 128 * XS_KC / 4; item += NSPLIT) {
         const int nc = item & 127, kq = item >> 7;
@@ -312,8 +321,8 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
         *reinterpret_cast<float4*>(sml + off) = make_float4(sl[0], sl[1], sl[2], sl[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      xs_arrive(&consumed[s % XS_NBUF]);
-      xs_arrive(&ready[s % XS_NSB]);
+      xs_arrive(&consumed[s % NBUF]);
+      xs_arrive(&ready[s % NSB]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -360,6 +369,41 @@ size_t xs_smem(int M, int K) {
   return ((size_t)(XS_NBUF + 2 * XS_NSB) * XS_CH + (size_t)4 * xs_mpad(M) * xs_kpad(K)) * sizeof(float) + 1024;
 }
 
+// Launch plan.  Default: every CTA holds all twiddle groups, 3-deep ring, 2 operand
+// buffers, per-chunk accumulators when K spans several chunks.  When the twiddles do not
+// fit (config 4's embed: 256 rows x 64 k, 256 KB), each CTA takes one output-row group of
+// its tiles (gsplit: that group's 128 KB of twiddles, X read once per group), a 2-deep ring
+// and one operand buffer, and — when the per-chunk accumulators would not fit TMEM — one
+// accumulator pair across the chunks (single).
+struct XsPlan {
+  bool ok = false;
+  int G = 1, NG = 0, gsplit = 0, single = 0, nbuf = XS_NBUF, nsb = XS_NSB, UC = 0, NACC = 1;
+  size_t smem = 0;
+};
+
+XsPlan xs_plan(int M, int K) {
+  XsPlan p;
+  xs_groups(M, p.G, p.NG);
+  const int Kpad = xs_kpad(K), nk = Kpad / XS_KC;
+  p.UC = xs_ucols(K, p.NG);
+  p.smem = xs_smem(M, K);
+  if (p.smem <= XS_SMEM_MAX && p.UC <= 512) {
+    p.ok = true;
+  } else if (p.G > 1) {
+    p.gsplit = 1;
+    p.nbuf = 2;
+    p.nsb = 1;
+    p.smem = ((size_t)(p.nbuf + 2 * p.nsb) * XS_CH + (size_t)4 * p.NG * Kpad) * sizeof(float) + 1024;
+    if (p.UC > 512 && nk > 1) {
+      p.single = 1;
+      p.UC = 2 * p.NG;
+    }
+    p.ok = p.smem <= XS_SMEM_MAX && p.UC <= 512;
+  }
+  p.NACC = 2 * p.UC <= 512 ? 2 : 1;
+  return p;
+}
+
 // TF32 round-to-nearest (ties away) of a float, on the host
 float xs_tf32(float x) {
   uint32_t b;
@@ -380,8 +424,9 @@ bool umma_xstage_fits(int M, int K, int N) {
   int G, NG;
   xs_groups(M, G, NG);
   // TMA: 16-byte row pitch (2N floats) and field stride (K N complex, the callers' layouts)
-  return M >= 1 && M <= 256 && K >= 1 && N % 2 == 0 && (1LL * K * N) % 2 == 0 && xs_smem(M, K) <= XS_SMEM_MAX &&
-         xs_ucols(K, NG) <= 512 && xs_encoder() != nullptr;
+  (void)NG;
+  return M >= 1 && M <= 256 && K >= 1 && N % 2 == 0 && (1LL * K * N) % 2 == 0 && xs_plan(M, K).ok &&
+         xs_encoder() != nullptr;
 }
 
 long long umma_xstage_twiddle_floats(int M, int K) { return 4LL * xs_mpad(M) * xs_kpad(K); }
@@ -420,34 +465,38 @@ void launch_umma_xstage(const float* tw, const float2* X, long long sX, float2* 
                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw EngineError(3, "umma x-stage: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  int G, NG;
-  xs_groups(M, G, NG);
+  const XsPlan pl = xs_plan(M, K);
+  if (!pl.ok) throw EngineError(3, "umma x-stage: no shared-memory / TMEM plan for this shape");
   const int T = nf * ((N2 + 127) / 128);
-  const int grid = std::min(kSMs, T);
-  const size_t smem = xs_smem(M, K);
-  // accumulator units double-buffered when they fit the 512 TMEM columns
-  const int UC = xs_ucols(K, NG);
-  const int NACC = 2 * UC <= 512 ? 2 : 1;
+  // gsplit: G CTAs per tile (one per output-row group), grid a multiple of G
+  const int grid = pl.gsplit ? std::min(kSMs / pl.G * pl.G, T * pl.G) : std::min(kSMs, T);
   auto go = [&](auto kern, int slot) {
-    static bool set[64][4] = {};
+    static bool set[64][8] = {};
     int dev = 0;
     LDDMM_CUDA(cudaGetDevice(&dev));
     if (!set[dev & 63][slot]) {
       LDDMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XS_SMEM_MAX));
       set[dev & 63][slot] = true;
     }
-    pdl_launch(kern, grid, XS_THREADS, smem, s, tm, tw, reinterpret_cast<float*>(C), 2 * sC, M, N2, Kpad, Mpad, nf,
-               NG, G, NACC, UC);
+    pdl_launch(kern, grid, XS_THREADS, pl.smem, s, tm, tw, reinterpret_cast<float*>(C), 2 * sC, M, N2, Kpad, Mpad,
+               nf, pl.NG, pl.G, pl.NACC, pl.UC, pl.gsplit, pl.single);
   };
-  const int cols = NACC * UC;
-  if (cols <= 64)
-    go(umma_xstage_kernel<64>, 0);
-  else if (cols <= 128)
-    go(umma_xstage_kernel<128>, 1);
-  else if (cols <= 256)
-    go(umma_xstage_kernel<256>, 2);
-  else
-    go(umma_xstage_kernel<512>, 3);
+  const int cols = pl.NACC * pl.UC;
+  if (!pl.gsplit) {
+    if (cols <= 64)
+      go(umma_xstage_kernel<64, XS_NBUF, XS_NSB>, 0);
+    else if (cols <= 128)
+      go(umma_xstage_kernel<128, XS_NBUF, XS_NSB>, 1);
+    else if (cols <= 256)
+      go(umma_xstage_kernel<256, XS_NBUF, XS_NSB>, 2);
+    else
+      go(umma_xstage_kernel<512, XS_NBUF, XS_NSB>, 3);
+  } else {
+    if (cols <= 256)
+      go(umma_xstage_kernel<256, 2, 1>, 4);
+    else
+      go(umma_xstage_kernel<512, 2, 1>, 5);
+  }
   LDDMM_LAUNCH_CHECK();
 }
 
