@@ -127,7 +127,10 @@ __global__ __launch_bounds__(XS_THREADS, 1) void umma_xstage_kernel(const __grid
   // split by warps 2-3; several chunks (project: K = Nx) -> the split dominates: 4
   // epilogue warps (4-7), split by warps 2-3 and 8-15
   const int nk = Kpad / XS_KC;
-  const int EW = (nk == 1 || single) ? 3 : 1;     // epilogue warps per TMEM lane quarter
+  // epilogue warps per TMEM lane quarter: 3 with one chunk per tile (drain-bound), 2 with
+  // one accumulator over several chunks (config 4's embed: 51 vs 64 us with 3), 1 with
+  // per-chunk accumulators (the split is the work)
+  const int EW = nk == 1 ? 3 : (single ? 2 : 1);
   const int NSPLIT = (XS_THREADS / 32 - 4 - 4 * EW + 2) * 32;  // split threads
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(xs_su32(&tmem_base_sh)),
