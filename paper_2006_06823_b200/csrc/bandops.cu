@@ -33,6 +33,39 @@ __global__ void axpby_kernel(long long n, double a, const double2* __restrict__ 
   }
 }
 
+// out = sum_j w_j x_j over count vectors x_j = x + j stride, accumulated in order j = 0, 1,
+// ... exactly as launch_scale(w_0) followed by launch_axpy(w_j, x_j, out, out) would (one
+// launch instead of count)
+struct WSum {
+  double w[64];
+};
+__global__ void weighted_sum_kernel(long long n, int count, const __grid_constant__ WSum ws,
+                                    const double2* __restrict__ x, long long stride, double2* __restrict__ out) {
+  pdl_prologue();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 x0 = x[i];
+    double2 r = make_double2(ws.w[0] * x0.x, ws.w[0] * x0.y);
+    for (int j = 1; j < count; ++j) {
+      const double2 xv = x[j * stride + i];
+      r = make_double2(ws.w[j] * xv.x + r.x, ws.w[j] * xv.y + r.y);
+    }
+    out[i] = r;
+  }
+}
+
+void launch_weighted_sum(long long n, int count, const double* w, const double2* x, long long stride, double2* out,
+                         cudaStream_t s) {
+  if (count > 64) {
+    launch_scale(n, w[0], x, out, s);
+    for (int j = 1; j < count; ++j) launch_axpy(n, w[j], x + j * stride, out, out, s);
+    return;
+  }
+  WSum ws;
+  for (int j = 0; j < count; ++j) ws.w[j] = w[j];
+  pdl_launch(weighted_sum_kernel, grid_for(n, 256, 4), 256, 0, s, n, count, ws, x, stride, out);
+  LDDMM_LAUNCH_CHECK();
+}
+
 void launch_axpy(long long n, double a, const double2* x, const double2* y, double2* out, cudaStream_t s) {
   pdl_launch(axpby_kernel, grid_for(n, 256, 4), 256, 0, s, n, a, x, 1.0, y, out);
   LDDMM_LAUNCH_CHECK();

@@ -830,8 +830,7 @@ void Engine::assemble_jacT_terms(const double2* U, const double2* Q, const doubl
   }
   // band part: acc = sum_i w_i q_i
   double2* acc = bt(6);
-  launch_scale(V, w[0], Q, acc, stream_);
-  for (int i = 1; i <= nt; ++i) launch_axpy(V, w[i], Q + i * V, acc, acc, stream_);
+  launch_weighted_sum(V, nt + 1, w.data(), Q, V, acc, stream_);
   // product part on the small grid, nodes 1..nt (u_0 = 0)
   const int per_chunk = std::min(5, fmax_small_ / 12);
   bool first = true;

@@ -150,6 +150,9 @@ void launch_circulant_axis_f64(const double* in, double* out, const double* D, i
 // ---- band algebra (fp64) ----------------------------------------------------------
 
 void launch_axpy(long long n, double a, const double2* x, const double2* y, double2* out, cudaStream_t s);
+// out = sum_{j < count} w_j (x + j stride), in order (= launch_scale + count - 1 launch_axpy)
+void launch_weighted_sum(long long n, int count, const double* w, const double2* x, long long stride, double2* out,
+                         cudaStream_t s);
 void launch_axpby(long long n, double a, const double2* x, double b, const double2* y, double2* out,
                   cudaStream_t s);
 void launch_scale(long long n, double a, const double2* x, double2* out, cudaStream_t s);
