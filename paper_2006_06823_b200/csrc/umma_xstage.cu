@@ -428,7 +428,7 @@ bool umma_xstage_fits(int M, int K, int N) {
   xs_groups(M, G, NG);
   // TMA: 16-byte row pitch (2N floats) and field stride (K N complex, the callers' layouts)
   (void)NG;
-  return M >= 1 && M <= 256 && K >= 1 && N % 2 == 0 && (1LL * K * N) % 2 == 0 && xs_plan(M, K).ok &&
+  return M >= 1 && M <= 256 && K >= 1 && N >= 64 && N % 2 == 0 && (1LL * K * N) % 2 == 0 && xs_plan(M, K).ok &&
          xs_encoder() != nullptr;
 }
 
@@ -458,6 +458,7 @@ void umma_xstage_twiddles_host(const float2* W, int M, int K, std::vector<float>
 // sX complex), C [nf][M][N] complex (field stride sC complex); tw from umma_xstage_twiddles_host
 void launch_umma_xstage(const float* tw, const float2* X, long long sX, float2* C, long long sC, int M, int N,
                         int K, int nf, cudaStream_t s) {
+  if (nf <= 0 || N <= 0) return;
   const int Mpad = xs_mpad(M), Kpad = xs_kpad(K), N2 = 2 * N;
   CUtensorMap tm;
   const cuuint64_t dims[3] = {(cuuint64_t)N2, (cuuint64_t)K, (cuuint64_t)nf};
